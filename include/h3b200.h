@@ -1,0 +1,128 @@
+/*
+ * h3b200 -- C ABI of the B200-native Hermite half-step (libh3b200.so).
+ *
+ * Drop-in boundary for the reference's grid kernels
+ * (reference: pkg/src/hermite3d/gridkernels.py).  The reference binds these
+ * through numba; the entry points below take exactly the arguments the
+ * reference passes from pipeline.half_step (pipeline.py:247-266) --
+ * src/dst DOF fields in the reference's rank-6 layout
+ * [m3][m2][m1][n3][n2][n1] (C order, field.py:80-93), the interpolation matrix
+ * h_mat (s x s), the derivative factors fac1..3 (s), the Horner stage factors
+ * cfac (q) and the gather offset off -- plus what a device needs: a CUDA
+ * stream, a slab range along x3, and a device flag for the fused
+ * finiteness check (pipeline.py:210-215).
+ *
+ * Conventions
+ *   - src/dst/coeff and every d_* pointer are DEVICE pointers; h_mat, fac*,
+ *     cfac are HOST arrays (tiny, copied into kernel parameters per call).
+ *   - All calls are asynchronous on `stream` (a cudaStream_t; NULL = legacy
+ *     default stream), reentrant, and keep no mutable global state.
+ *   - Return 0 on success, a positive cudaError_t on a CUDA error, or a
+ *     negative H3_ERR_* code for invalid arguments.  No C++ exception crosses
+ *     the ABI.
+ *   - Cells [z_begin, z_end) along x3 are processed.  With periodic_z != 0
+ *     node planes wrap modulo M3 (single-GPU field).  With periodic_z == 0 the
+ *     planes -1 and M3 are read from memory directly before / after the field
+ *     (ghost planes filled by the slab halo exchange).
+ *   - d_first_bad (may be NULL) receives atomicMin of the linear node index
+ *     (m3*M2 + m2)*M1 + m1 of every destination node holding a non-finite
+ *     value; initialise it to H3_NO_BAD_NODE.  d_guard (may be NULL): when it
+ *     holds anything other than H3_NO_BAD_NODE the call does no work (the
+ *     reference never runs a half step after an unstable one).
+ */
+#ifndef H3B200_H
+#define H3B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define H3_NO_BAD_NODE 0xFFFFFFFFFFFFFFFFull
+
+/* kernel variants */
+#define H3_VARIANT_AUTO 0      /* separable when q >= 3(2N+1) (exact), else literal   */
+#define H3_VARIANT_LITERAL 1   /* bit-identical to the reference (no FMA, same order)  */
+#define H3_VARIANT_SEPARABLE 2 /* node-factorised exact evolution, HBM-bound fast path */
+
+/* negative status codes */
+#define H3_ERR_ARG -1     /* null pointer, bad size, bad offset or slab range   */
+#define H3_ERR_ORDER -2   /* order_n outside [0, h3_max_order()]                */
+#define H3_ERR_STAGES -3  /* q outside [1, h3_max_stages()], or separable with q < 3(2N+1) */
+#define H3_ERR_VARIANT -4 /* variant not available for this precision/kernel    */
+
+/* Replaces gridkernels.fused_pass(src, dst, h_mat, fac1, fac2, fac3, cfac, tiles, off)
+ * (reference gridkernels.py:121-139; called from pipeline.py:251).  `tiles` has
+ * no device analogue (results never depend on tiling, pipeline.py:11-14). */
+int h3_fused_pass(const double* src, double* dst, int64_t M1, int64_t M2, int64_t M3,
+                  int order_n, const double* h_mat, const double* fac1, const double* fac2,
+                  const double* fac3, const double* cfac, int q, int off, int64_t z_begin,
+                  int64_t z_end, int periodic_z, int variant, void* stream,
+                  unsigned long long* d_first_bad, const unsigned long long* d_guard);
+
+/* precision="single" (field.py:30): literal variant only. */
+int h3_fused_pass_f32(const float* src, float* dst, int64_t M1, int64_t M2, int64_t M3,
+                      int order_n, const float* h_mat, const float* fac1, const float* fac2,
+                      const float* fac3, const float* cfac, int q, int off, int64_t z_begin,
+                      int64_t z_end, int periodic_z, int variant, void* stream,
+                      unsigned long long* d_first_bad, const unsigned long long* d_guard);
+
+/* Replaces gridkernels.recon_pass(src, coeff, h_mat, tiles, off) (gridkernels.py:142-160;
+ * pipeline.py:262).  coeff holds only the cells [z_begin, z_end) (slab chunk):
+ * coeff[(c3 - z_begin)][c2][c1][s][s][s].  variant LITERAL = reference summation
+ * order without FMA; SEPARABLE/AUTO = same sweeps with FMA. */
+int h3_recon_pass(const double* src, double* coeff, int64_t M1, int64_t M2, int64_t M3,
+                  int order_n, const double* h_mat, int off, int64_t z_begin, int64_t z_end,
+                  int periodic_z, int variant, void* stream, const unsigned long long* d_guard);
+int h3_recon_pass_f32(const float* src, float* coeff, int64_t M1, int64_t M2, int64_t M3,
+                      int order_n, const float* h_mat, int off, int64_t z_begin, int64_t z_end,
+                      int periodic_z, int variant, void* stream, const unsigned long long* d_guard);
+
+/* Replaces gridkernels.evolve_pass(coeff, dst, fac1, fac2, fac3, cfac, tiles)
+ * (gridkernels.py:163-182; pipeline.py:265).  coeff is chunk-relative as above;
+ * dst nodes of cells [z_begin, z_end) are written. */
+int h3_evolve_pass(const double* coeff, double* dst, int64_t M1, int64_t M2, int64_t M3,
+                   int order_n, const double* fac1, const double* fac2, const double* fac3,
+                   const double* cfac, int q, int64_t z_begin, int64_t z_end, int variant,
+                   void* stream, unsigned long long* d_first_bad, const unsigned long long* d_guard);
+int h3_evolve_pass_f32(const float* coeff, float* dst, int64_t M1, int64_t M2, int64_t M3,
+                       int order_n, const float* fac1, const float* fac2, const float* fac3,
+                       const float* cfac, int q, int64_t z_begin, int64_t z_end, int variant,
+                       void* stream, unsigned long long* d_first_bad,
+                       const unsigned long long* d_guard);
+
+/* Host helper: the separable operators the fast path uses, derived from the
+ * reference's own arguments (delta = cfac[0], 1/h_k = fac_k[0]) in extended
+ * precision and rounded once.  A_out: [3][n][2n] (A_k = S_k[0:n,:] H),
+ * S_out: [3][n][2n] (S_k[m][j] = C(j,m) (delta/h_k)^(j-m)).  Either may be NULL. */
+int h3_separable_operators(int order_n, const double* h_mat, const double* fac1,
+                           const double* fac2, const double* fac3, const double* cfac, int q,
+                           double* A_out, double* S_out);
+
+/* Device initial data (reference problems.py:150-175): dst[m3][m2][m1][j3][j2][j1] =
+ * sum_t t3[t][m3][j3] * t2[t][m2][j2] * t1[t][m1][j1]; t_k are DEVICE tables
+ * [nterms][M_k][n] of per-axis scaled derivatives (problems.py:47-54). */
+int h3_init_separable(double* dst, int64_t M1, int64_t M2, int64_t M3, int order_n, int nterms,
+                      const double* t1, const double* t2, const double* t3, void* stream);
+
+/* Device error norms (reference problems.py:202-213): d_out[0] = max |u - exact|,
+ * d_out[1] = sum (u - exact)^2 over node values, exact = sum_t e3[t][m3] e2[t][m2] e1[t][m1]
+ * (DEVICE tables [nterms][M_k]).  d_partials: scratch of 2*n_partials doubles. */
+int h3_error_norms(const double* field, int64_t M1, int64_t M2, int64_t M3, int order_n,
+                   int nterms, const double* e1, const double* e2, const double* e3,
+                   double* d_partials, int64_t n_partials, double* d_out, void* stream);
+
+/* Standalone finiteness scan (reference pipeline.py:210-215). */
+int h3_check_finite(const double* field, int64_t M1, int64_t M2, int64_t M3, int order_n,
+                    unsigned long long* d_first_bad, void* stream);
+
+const char* h3_version(void);
+const char* h3_error_string(int status);
+int h3_max_order(void);
+int h3_max_stages(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* H3B200_H */

@@ -1,0 +1,71 @@
+// Internal launcher declarations shared by the CUDA translation units and the
+// C-ABI layer (h3_capi.cu).  Not part of the public ABI (see include/h3b200.h).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "h3_common.cuh"
+
+namespace h3 {
+
+// Grid geometry of one launch.  Cells [z_begin, z_end) along x3 are processed;
+// x1/x2 are always periodic.  Along x3 node planes wrap modulo M3 when
+// periodic_z != 0, otherwise planes -1 and M3 are ghost planes stored
+// contiguously before/after the field (slab decomposition).
+struct Dims {
+    int64_t M1, M2, M3;
+    int64_t z_begin, z_end;
+    int periodic_z;
+};
+
+// Literal (bit-faithful) operator bundle: exactly the reference's factor arrays
+// (pipeline.py:197-207), carried as kernel parameters (constant bank).
+template <typename T, int N>
+struct LitOps {
+    static constexpr int S = 2 * N + 2;
+    T H[S * S];
+    T f1[S], f2[S], f3[S];
+    T cf[H3_MAX_STAGES];
+    int q;
+};
+
+// Separable operator bundle: per-axis node-to-node maps A_k = S_k[0:n, :] H
+// (n x 2n, [axis][m][a*n + j]) and the shift rows S_k[0:n, :] (n x s).
+template <int N>
+struct SepOps {
+    static constexpr int n = N + 1, S = 2 * N + 2;
+    double A[3][n][S];
+    double Sh[3][n][S];
+};
+
+// Host operator math (h3_capi.cu): fills A and S from the reference's own
+// arguments (N, H, delta = cfac[0], 1/h_k = fac_k[0]) in extended precision.
+void build_separable(int order_n, const double* h_mat, const double* fac1, const double* fac2,
+                     const double* fac3, double delta, double* A /*3*n*s*/, double* Sh /*3*n*s*/);
+
+// ---- launchers (return cudaError_t as int) --------------------------------
+template <typename T>
+int literal_launch(int mode /*0 fused,1 recon,2 evolve*/, bool fast, const T* in, T* out,
+                   const Dims& d, int order_n, const T* H, const T* f1, const T* f2,
+                   const T* f3, const T* cf, int q, int off, cudaStream_t st,
+                   unsigned long long* first_bad, const unsigned long long* guard);
+
+int sep_fused_launch(const double* src, double* dst, const Dims& d, int order_n,
+                     const double* A, int off, cudaStream_t st, unsigned long long* first_bad,
+                     const unsigned long long* guard);
+int sep_evolve_launch(const double* coeff, double* dst, const Dims& d, int order_n,
+                      const double* Sh, cudaStream_t st, unsigned long long* first_bad,
+                      const unsigned long long* guard);
+
+int init_separable_launch(double* dst, int64_t M1, int64_t M2, int64_t M3, int order_n,
+                          int nterms, const double* t1, const double* t2, const double* t3,
+                          cudaStream_t st);
+int error_norms_launch(const double* field, int64_t M1, int64_t M2, int64_t M3, int order_n,
+                       int nterms, const double* e1, const double* e2, const double* e3,
+                       double* d_partials, int64_t n_partials, double* d_out, cudaStream_t st);
+int check_finite_launch(const double* field, int64_t M1, int64_t M2, int64_t M3, int order_n,
+                        unsigned long long* first_bad, cudaStream_t st);
+
+int num_sms();
+
+}  // namespace h3

@@ -1,0 +1,366 @@
+// Separable (node-factorised) Hermite half-step kernels -- the B200 fast path.
+//
+// For q >= 3(2N+1) stages the reference's local evolution is exact
+// (kernels.py:30-35; pinned by the reference's
+// test_exact_local_evolution_matches_shift, pkg/tests/test_kernels.py:184-199),
+// so reconstruct+evolve+truncate of one cell equals the exact translation
+//     out(c) = sum_{a in {0,1}^3} (A3^{a3} (x) A2^{a2} (x) A1^{a1}) u(c + off + a),
+// with A_k = S_k[0:n, :] H (n x 2n), S_k[m][j] = C(j,m) (delta/h_k)^(j-m).
+// Applied axis by axis that is 6 n^4 FMAs per node instead of the literal
+// ~q s^3 * 8: 3 flop/B at N=3, i.e. HBM-bound on B200.
+//
+// sep_fused_kernel: CTA = TX x TY cells in (x1, x2), marching along x3 over a
+// chunk of cell planes.  Per node plane:
+//   1. the (TX+1) x (TY+1) node tile is staged into shared memory with
+//      cp.async (double-buffered: plane p+1 streams in while p is computed);
+//   2. pass x1 (smem -> smem): W[ly][ix] = A1^0 U[ly][ix] + A1^1 U[ly][ix+1];
+//   3. pass x2 (smem -> registers) and pass x3 (registers, "register
+//      rolling" across planes as in the paper): each thread owns
+//      one (cell, m1) column and accumulates the two x3 contributions of the
+//      plane into the finishing cell (a3 = 1) and the next cell (a3 = 0);
+//   4. the finished cell plane is stored with a fused finiteness check.
+// HBM traffic: each node block is read once and written once per half step
+// (32 B per DOF-update); the tile halo is re-read from L2.
+#include "h3_launch.h"
+
+namespace h3 {
+
+template <int N> struct SepTile;
+// TX, TY: cells per CTA; PAD: doubles of padding per node block in smem.
+template <> struct SepTile<0> { static constexpr int TX = 32, TY = 8, PAD = 1; };
+template <> struct SepTile<1> { static constexpr int TX = 16, TY = 8, PAD = 2; };
+template <> struct SepTile<2> { static constexpr int TX = 8, TY = 8, PAD = 1; };
+template <> struct SepTile<3> { static constexpr int TX = 8, TY = 8, PAD = 4; };
+template <> struct SepTile<4> { static constexpr int TX = 8, TY = 4, PAD = 1; };
+template <> struct SepTile<5> { static constexpr int TX = 8, TY = 4, PAD = 2; };
+
+template <int N, int TX, int TY, int PAD>
+struct SepGeom {
+    static constexpr int n = N + 1, n2 = n * n, n3 = n2 * n;
+    static constexpr int NX = TX + 1, NY = TY + 1;
+    static constexpr int NS = n3 + PAD;                 // node stride in smem (doubles)
+    static constexpr int THREADS = TX * TY * n;
+    static constexpr int VEC = (n3 % 2 == 0 && NS % 2 == 0) ? 2 : 1;  // doubles per cp.async
+    static constexpr int CPN = n3 / VEC;                 // copies per node
+    static constexpr int NCOPY = NY * NX * CPN;
+    static constexpr int L1 = NY * TX * n2;              // pass-x1 lines
+    static constexpr int R1 = (L1 + THREADS - 1) / THREADS;
+    static constexpr size_t U_DOUBLES = (size_t)NY * NX * NS;
+    static constexpr size_t W_DOUBLES = (size_t)NY * TX * NS;
+    static constexpr size_t SMEM = (2 * U_DOUBLES + W_DOUBLES) * sizeof(double);
+};
+
+template <int N, int TX, int TY, int PAD>
+__global__ void __launch_bounds__(SepGeom<N, TX, TY, PAD>::THREADS)
+sep_fused_kernel(const double* __restrict__ src, double* __restrict__ dst, Dims d, int off,
+                 int zchunk, const __grid_constant__ SepOps<N> p,
+                 unsigned long long* first_bad, const unsigned long long* guard) {
+    using G = SepGeom<N, TX, TY, PAD>;
+    constexpr int n = G::n, n2 = G::n2, n3 = G::n3, NX = G::NX, NS = G::NS;
+    if (guarded_out(guard, first_bad)) return;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    double* U0 = reinterpret_cast<double*>(smem_raw);
+    double* U1 = U0 + G::U_DOUBLES;
+    double* W = U1 + G::U_DOUBLES;
+
+    const int tid = threadIdx.x;
+    const int M1 = (int)d.M1, M2 = (int)d.M2;
+    const int cx0 = blockIdx.x * TX, cy0 = blockIdx.y * TY;
+    const int64_t zc0 = d.z_begin + (int64_t)blockIdx.z * zchunk;
+    const int64_t zc1 = min(zc0 + (int64_t)zchunk, d.z_end);
+    const int P = (int)(zc1 - zc0) + 1;  // node planes touched by this chunk
+    const int64_t plane_elems = (int64_t)M1 * M2 * n3;
+
+    auto issue = [&](int pl, double* Ub) {
+        const int64_t gz = zplane(zc0 + off + pl, d.M3, d.periodic_z);
+        const double* base = src + gz * plane_elems;
+        for (int e = tid; e < G::NCOPY; e += G::THREADS) {
+            const int ly = e / (NX * G::CPN);
+            const int r = e - ly * (NX * G::CPN);
+            const int lx = r / G::CPN;
+            const int pc = r - lx * G::CPN;
+            int gx = cx0 + off + lx, gy = cy0 + off + ly;
+            if (gx < 0) gx += M1; else if (gx >= M1) gx %= M1;
+            if (gy < 0) gy += M2; else if (gy >= M2) gy %= M2;
+            const double* g = base + ((int64_t)gy * M1 + gx) * n3 + pc * G::VEC;
+            double* s = Ub + (ly * NX + lx) * NS + pc * G::VEC;
+            if (G::VEC == 2) cp_async16(s, g); else cp_async8(s, g);
+        }
+    };
+
+    // pass x2/x3 ownership: (m1, ix, iy)
+    const int m1 = tid % n;
+    const int ix = (tid / n) % TX;
+    const int iy = tid / (n * TX);
+    const int cx = cx0 + ix, cy = cy0 + iy;
+    const bool owns = (cx < M1) && (cy < M2);
+
+    double accP[n][n];  // cell finishing at this plane (a3 = 1 contribution pending)
+#pragma unroll
+    for (int a = 0; a < n; ++a)
+#pragma unroll
+        for (int b = 0; b < n; ++b) accP[a][b] = 0.0;
+
+    issue(0, U0);
+    cp_async_commit();
+    for (int pl = 0; pl < P; ++pl) {
+        double* Ub = (pl & 1) ? U1 : U0;
+        if (pl + 1 < P) issue(pl + 1, (pl & 1) ? U0 : U1);
+        cp_async_commit();
+        cp_async_wait<1>();
+        __syncthreads();
+
+        // ---- pass x1: W[ly][ix][j3][j2][m1] -------------------------------------------
+#pragma unroll
+        for (int r = 0; r < G::R1; ++r) {
+            const int l = tid + r * G::THREADS;
+            if (l < G::L1) {
+                const int j32 = l % n2;
+                const int rest = l / n2;
+                const int lix = rest % TX, ly = rest / TX;
+                const double* u0 = Ub + (ly * NX + lix) * NS + j32 * n;
+                const double* u1 = u0 + NS;
+                double a[n], b[n];
+#pragma unroll
+                for (int j = 0; j < n; ++j) { a[j] = u0[j]; b[j] = u1[j]; }
+                double* wout = W + (ly * TX + lix) * NS + j32 * n;
+#pragma unroll
+                for (int m = 0; m < n; ++m) {
+                    double acc = p.A[0][m][0] * a[0];
+#pragma unroll
+                    for (int j = 1; j < n; ++j) acc = fma(p.A[0][m][j], a[j], acc);
+#pragma unroll
+                    for (int j = 0; j < n; ++j) acc = fma(p.A[0][m][n + j], b[j], acc);
+                    wout[m] = acc;
+                }
+            }
+        }
+        __syncthreads();
+
+        // ---- pass x2 + x3 ----------------------------------------------------------------
+        {
+            const double* w0 = W + (iy * TX + ix) * NS + m1;
+            const double* w1 = w0 + TX * NS;
+            double accN[n][n];
+#pragma unroll
+            for (int j3 = 0; j3 < n; ++j3) {
+                double a[n], b[n];
+#pragma unroll
+                for (int j = 0; j < n; ++j) { a[j] = w0[(j3 * n + j) * n]; b[j] = w1[(j3 * n + j) * n]; }
+                double v[n];
+#pragma unroll
+                for (int m = 0; m < n; ++m) {
+                    double acc = p.A[1][m][0] * a[0];
+#pragma unroll
+                    for (int j = 1; j < n; ++j) acc = fma(p.A[1][m][j], a[j], acc);
+#pragma unroll
+                    for (int j = 0; j < n; ++j) acc = fma(p.A[1][m][n + j], b[j], acc);
+                    v[m] = acc;
+                }
+#pragma unroll
+                for (int m3 = 0; m3 < n; ++m3)
+#pragma unroll
+                    for (int m2 = 0; m2 < n; ++m2) {
+                        accP[m3][m2] = fma(p.A[2][m3][n + j3], v[m2], accP[m3][m2]);
+                        accN[m3][m2] = j3 == 0 ? p.A[2][m3][0] * v[m2]
+                                               : fma(p.A[2][m3][j3], v[m2], accN[m3][m2]);
+                    }
+            }
+            if (pl > 0 && owns) {
+                const int64_t c3 = zc0 + pl - 1;
+                const int64_t node = (c3 * M2 + cy) * (int64_t)M1 + cx;
+                double* o = dst + node * n3 + m1;
+                bool bad = false;
+#pragma unroll
+                for (int m3 = 0; m3 < n; ++m3)
+#pragma unroll
+                    for (int m2 = 0; m2 < n; ++m2) {
+                        o[(m3 * n + m2) * n] = accP[m3][m2];
+                        bad |= !isfinite(accP[m3][m2]);
+                    }
+                if (bad) flag_bad(first_bad, node);
+            }
+#pragma unroll
+            for (int a = 0; a < n; ++a)
+#pragma unroll
+                for (int b = 0; b < n; ++b) accP[a][b] = accN[a][b];
+        }
+        __syncthreads();
+    }
+}
+
+template <int N>
+static int sep_fused_n(const double* src, double* dst, const Dims& d, const double* A, int off,
+                       cudaStream_t st, unsigned long long* first_bad,
+                       const unsigned long long* guard) {
+    using T = SepTile<N>;
+    using G = SepGeom<N, T::TX, T::TY, T::PAD>;
+    const int64_t nz = d.z_end - d.z_begin;
+    if (nz <= 0 || d.M1 <= 0 || d.M2 <= 0) return 0;
+    SepOps<N> ops;
+    for (int k = 0; k < 3; ++k)
+        for (int m = 0; m < G::n; ++m)
+            for (int c = 0; c < 2 * G::n; ++c) {
+                ops.A[k][m][c] = A[(k * G::n + m) * 2 * G::n + c];
+                ops.Sh[k][m][c] = 0.0;
+            }
+    auto kern = sep_fused_kernel<N, T::TX, T::TY, T::PAD>;
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)G::SMEM);
+    if (e != cudaSuccess) return (int)e;
+    int per_sm = 0;
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, G::THREADS, G::SMEM);
+    if (e != cudaSuccess) return (int)e;
+    const int64_t gx = (d.M1 + T::TX - 1) / T::TX, gy = (d.M2 + T::TY - 1) / T::TY;
+    // enough CTAs for ~4 waves; split the z march only when the x-y tiling is too coarse
+    const int64_t want = (int64_t)num_sms() * (per_sm > 0 ? per_sm : 1) * 4;
+    int64_t zsplit = (want + gx * gy - 1) / (gx * gy);
+    int64_t zchunk = (nz + zsplit - 1) / zsplit;
+    if (zchunk < 8) zchunk = nz < 8 ? nz : 8;
+    const int64_t gz = (nz + zchunk - 1) / zchunk;
+    dim3 grid((unsigned)gx, (unsigned)gy, (unsigned)gz);
+    kern<<<grid, G::THREADS, G::SMEM, st>>>(src, dst, d, off, (int)zchunk, ops, first_bad, guard);
+    return (int)cudaGetLastError();
+}
+
+int sep_fused_launch(const double* src, double* dst, const Dims& d, int order_n, const double* A,
+                     int off, cudaStream_t st, unsigned long long* first_bad,
+                     const unsigned long long* guard) {
+    switch (order_n) {
+        case 0: return sep_fused_n<0>(src, dst, d, A, off, st, first_bad, guard);
+        case 1: return sep_fused_n<1>(src, dst, d, A, off, st, first_bad, guard);
+        case 2: return sep_fused_n<2>(src, dst, d, A, off, st, first_bad, guard);
+        case 3: return sep_fused_n<3>(src, dst, d, A, off, st, first_bad, guard);
+        case 4: return sep_fused_n<4>(src, dst, d, A, off, st, first_bad, guard);
+        case 5: return sep_fused_n<5>(src, dst, d, A, off, st, first_bad, guard);
+    }
+    return (int)cudaErrorInvalidValue;
+}
+
+// ---------------------------------------------------------------------------------------
+// Separable evolution of a materialised coefficient field (two-kernel fast path):
+// out[m3][m2][m1] = sum S3[m3][i3] S2[m2][i2] S1[m1][i1] coeff[i3][i2][i1], applied axis by
+// axis (s^3 n + s^2 n^2 + s n^3 FMAs per cell).  S_k are the exact shift rows of
+// exp(delta d/dx_k); equal to the reference's q-stage Horner for q >= 3(2N+1).
+// CTA = CPB consecutive cells (contiguous in the chunked coefficient field).
+template <int N>
+constexpr int ev_cpb() { return N <= 1 ? 16 : (N <= 3 ? 4 : 2); }
+
+template <int N, int CPB>
+__global__ void __launch_bounds__(CPB*(2 * N + 2) * (2 * N + 2))
+sep_evolve_kernel(const double* __restrict__ coeff, double* __restrict__ dst, Dims d,
+                  const __grid_constant__ SepOps<N> p, unsigned long long* first_bad,
+                  const unsigned long long* guard) {
+    constexpr int n = N + 1, S = 2 * n, S2 = S * S, S3 = S2 * S, n3 = n * n * n;
+    constexpr int THREADS = CPB * S2;
+    if (guarded_out(guard, first_bad)) return;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    double* C = reinterpret_cast<double*>(smem_raw);  // CPB * S3
+    double* T1 = C + CPB * S3;                          // CPB * S*S*n   [c][i3][i2][m1]
+    double* T2 = T1 + CPB * S2 * n;                     // CPB * S*n*n   [c][i3][m2][m1]
+
+    const int64_t nxy = d.M1 * d.M2;
+    const int64_t total = (d.z_end - d.z_begin) * nxy;
+    const int64_t cell0 = (int64_t)blockIdx.x * CPB;
+    const int ncell = (int)min((int64_t)CPB, total - cell0);
+    const int tid = threadIdx.x;
+    {
+        const double* g = coeff + cell0 * S3;
+        const int count = ncell * S3 / 2;  // S3 is even
+        for (int e = tid; e < count; e += THREADS) cp_async16(C + 2 * e, g + 2 * e);
+        cp_async_commit();
+        cp_async_wait<0>();
+    }
+    __syncthreads();
+    // pass x1: lines (c, i3, i2) -> n outputs m1
+    {
+        const int c = tid / S2, line = tid % S2;
+        const double* in = C + c * S3 + line * S;
+        double u[S];
+#pragma unroll
+        for (int k = 0; k < S; ++k) u[k] = in[k];
+#pragma unroll
+        for (int m = 0; m < n; ++m) {
+            double acc = p.Sh[0][m][0] * u[0];
+#pragma unroll
+            for (int k = 1; k < S; ++k) acc = fma(p.Sh[0][m][k], u[k], acc);
+            T1[(c * S2 + line) * n + m] = acc;
+        }
+    }
+    __syncthreads();
+    // pass x2: lines (c, i3, m1) -> n outputs m2
+    for (int l = tid; l < CPB * S * n; l += THREADS) {
+        const int c = l / (S * n), r = l % (S * n), i3 = r / n, mm1 = r % n;
+        double u[S];
+#pragma unroll
+        for (int k = 0; k < S; ++k) u[k] = T1[((c * S + i3) * S + k) * n + mm1];
+#pragma unroll
+        for (int m = 0; m < n; ++m) {
+            double acc = p.Sh[1][m][0] * u[0];
+#pragma unroll
+            for (int k = 1; k < S; ++k) acc = fma(p.Sh[1][m][k], u[k], acc);
+            T2[((c * S + i3) * n + m) * n + mm1] = acc;
+        }
+    }
+    __syncthreads();
+    // pass x3: lines (c, m2, m1) -> n outputs m3, stored to the destination node
+    for (int l = tid; l < CPB * n * n; l += THREADS) {
+        const int c = l / (n * n), r = l % (n * n);
+        if (c >= ncell) continue;
+        double u[S];
+#pragma unroll
+        for (int k = 0; k < S; ++k) u[k] = T2[(c * S + k) * n * n + r];
+        const int64_t cell = cell0 + c;
+        const int64_t crel3 = cell / nxy, rem = cell - crel3 * nxy;
+        const int64_t node = ((d.z_begin + crel3) * d.M2 + rem / d.M1) * d.M1 + rem % d.M1;
+        double* o = dst + node * n3 + r;
+        bool bad = false;
+#pragma unroll
+        for (int m = 0; m < n; ++m) {
+            double acc = p.Sh[2][m][0] * u[0];
+#pragma unroll
+            for (int k = 1; k < S; ++k) acc = fma(p.Sh[2][m][k], u[k], acc);
+            o[m * n * n] = acc;
+            bad |= !isfinite(acc);
+        }
+        if (bad) flag_bad(first_bad, node);
+    }
+}
+
+template <int N>
+static int sep_evolve_n(const double* coeff, double* dst, const Dims& d, const double* Sh,
+                        cudaStream_t st, unsigned long long* first_bad,
+                        const unsigned long long* guard) {
+    constexpr int n = N + 1, S = 2 * n, S2 = S * S, S3 = S2 * S, CPB = ev_cpb<N>();
+    const int64_t total = (d.z_end - d.z_begin) * d.M1 * d.M2;
+    if (total <= 0) return 0;
+    SepOps<N> ops;
+    for (int k = 0; k < 3; ++k)
+        for (int m = 0; m < n; ++m)
+            for (int c = 0; c < S; ++c) {
+                ops.Sh[k][m][c] = Sh[(k * n + m) * S + c];
+                ops.A[k][m][c] = 0.0;
+            }
+    const size_t smem = (size_t)CPB * (S3 + S2 * n + S * n * n) * sizeof(double);
+    auto kern = sep_evolve_kernel<N, CPB>;
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return (int)e;
+    const int64_t blocks = (total + CPB - 1) / CPB;
+    kern<<<(unsigned)blocks, CPB * S2, smem, st>>>(coeff, dst, d, ops, first_bad, guard);
+    return (int)cudaGetLastError();
+}
+
+int sep_evolve_launch(const double* coeff, double* dst, const Dims& d, int order_n,
+                      const double* Sh, cudaStream_t st, unsigned long long* first_bad,
+                      const unsigned long long* guard) {
+    switch (order_n) {
+        case 0: return sep_evolve_n<0>(coeff, dst, d, Sh, st, first_bad, guard);
+        case 1: return sep_evolve_n<1>(coeff, dst, d, Sh, st, first_bad, guard);
+        case 2: return sep_evolve_n<2>(coeff, dst, d, Sh, st, first_bad, guard);
+        case 3: return sep_evolve_n<3>(coeff, dst, d, Sh, st, first_bad, guard);
+        case 4: return sep_evolve_n<4>(coeff, dst, d, Sh, st, first_bad, guard);
+        case 5: return sep_evolve_n<5>(coeff, dst, d, Sh, st, first_bad, guard);
+    }
+    return (int)cudaErrorInvalidValue;
+}
+
+}  // namespace h3

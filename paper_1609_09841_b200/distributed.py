@@ -1,0 +1,176 @@
+"""Slab decomposition of the periodic grid along x3 with a one-plane halo per half step.
+
+The reference has no multi-process path; this module is
+the B200 scaling layer of SURVEY.md 8(e).  x3 is the outermost index of the
+DOF layout [m3][m2][m1][n3][n2][n1], so a node plane is one contiguous
+M1*M2*(N+1)^3 block.
+
+Each rank stores its L local planes between two ghost planes:
+    buf[0] = ghost_lo, buf[1 .. L] = local planes, buf[L+1] = ghost_hi.
+A half step needs ONE neighbour plane, and the direction alternates with
+the gather offset (reference gridkernels.py:46, g = c + off + a):
+    off =  0 (primary -> dual): cell c needs nodes c, c+1  -> ghost_hi = first
+             local plane of rank+1 (send my first plane to rank-1);
+    off = -1 (dual -> primary): cell c needs nodes c-1, c  -> ghost_lo = last
+             local plane of rank-1 (send my last plane to rank+1).
+The ranks form a periodic ring.  On the GPU the exchange is an NCCL
+send/recv pair (over NVLink/NVSwitch) issued before the interior cell planes
+are launched, so it overlaps with them; the one boundary cell plane that
+reads the ghost is launched after the exchange completes.  The kernels read
+the ghost planes directly (h3_fused_pass with periodic_z = 0).
+"""
+
+from __future__ import annotations
+
+import ctypes
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+from . import _native
+from .field import GridSpec
+from .pipeline import InstabilityError, OperatorSet, StepConfig, _factor_arrays, _node_of, _ptr, select_dt
+
+__all__ = ["slab_bounds", "halo_plan", "exchange_halo", "SlabSolver"]
+
+
+def slab_bounds(m3: int, world: int, rank: int) -> tuple[int, int]:
+    """Planes [z0, z1) owned by `rank` (the first m3 % world ranks get one extra)."""
+    base, extra = divmod(m3, world)
+    z0 = rank * base + min(rank, extra)
+    return z0, z0 + base + (1 if rank < extra else 0)
+
+
+def halo_plan(off: int, rank: int, world: int, local_planes: int):
+    """(send_buf_index, send_to, recv_buf_index, recv_from) for one half step."""
+    nxt, prv = (rank + 1) % world, (rank - 1) % world
+    if off == 0:
+        return 1, prv, local_planes + 1, nxt
+    if off == -1:
+        return local_planes, nxt, 0, prv
+    raise ValueError(f"off must be 0 or -1, got {off}")
+
+
+def exchange_halo(buf: torch.Tensor, off: int, group=None, async_op: bool = False):
+    """Fill the ghost plane a half step with offset `off` reads (see module doc).
+
+    `buf` has shape (L + 2, ...) with the ghost planes at both ends.  Works for
+    CUDA tensors (NCCL) and CPU tensors (gloo).  Returns the list of pending
+    works when async_op (empty when the exchange was a local copy).
+    """
+    world = dist.get_world_size(group) if dist.is_initialized() else 1
+    rank = dist.get_rank(group) if dist.is_initialized() else 0
+    local = buf.shape[0] - 2
+    send_i, send_to, recv_i, recv_from = halo_plan(off, rank, world, local)
+    if world == 1:
+        buf[recv_i].copy_(buf[send_i])
+        return []
+    to_g = dist.get_global_rank(group, send_to) if group is not None else send_to
+    from_g = dist.get_global_rank(group, recv_from) if group is not None else recv_from
+    ops = [dist.P2POp(dist.isend, buf[send_i], to_g, group),
+           dist.P2POp(dist.irecv, buf[recv_i], from_g, group)]
+    works = dist.batch_isend_irecv(ops)
+    if async_op:
+        return works
+    for w in works:
+        w.wait()
+    return []
+
+
+class SlabSolver:
+    """Distributed full steps of a periodic field, one x3 slab per rank (one GPU per rank).
+
+    Fields are stored with ghost planes (see module doc); `state` / `scratch`
+    return views of the local planes.  Used by bench.py for the 2/4/8-GPU runs.
+    """
+
+    def __init__(self, global_cells, order_n: int, cfg: StepConfig, lengths=(1.0, 1.0, 1.0), group=None):
+        self.group = group
+        self.world = dist.get_world_size(group) if dist.is_initialized() else 1
+        self.rank = dist.get_rank(group) if dist.is_initialized() else 0
+        self.grid = GridSpec(tuple(global_cells), tuple(lengths))
+        self.order_n = order_n
+        self.cfg = cfg
+        m1, m2, m3 = self.grid.cells_per_axis
+        self.z0, self.z1 = slab_bounds(m3, self.world, self.rank)
+        self.local = self.z1 - self.z0
+        if self.local < 2:
+            raise ValueError("each rank needs at least two x3 planes")
+        n = order_n + 1
+        shape = (self.local + 2, m2, m1, n, n, n)
+        self.bufs = [torch.zeros(shape, dtype=torch.float64, device="cuda") for _ in range(2)]
+        self.ops = OperatorSet.for_grid(self.grid, order_n)
+        self.dt = select_dt(self.grid, cfg)
+        self.flags = torch.full((2,), -1, dtype=torch.int64, device="cuda")
+        self.kernel_events = []
+        self.launches_per_step = 4
+        q = cfg.stages(order_n)
+        self._fac = _factor_arrays(self.ops, np.float64, self.dt / 2, q)
+        self._q = q
+        if cfg.mode != "fused":
+            raise NotImplementedError("SlabSolver runs the fused half step")
+
+    @property
+    def state(self) -> torch.Tensor:
+        return self.bufs[0][1:-1]
+
+    @property
+    def scratch(self) -> torch.Tensor:
+        return self.bufs[1][1:-1]
+
+    def init(self, ic) -> None:
+        """Device initial data of this rank's planes (global x3 coordinates)."""
+        from .problems import init_tables, launch_init
+        t1, t2, t3 = init_tables(ic, self.grid, self.order_n)
+        m1, m2, _ = self.grid.cells_per_axis
+        launch_init(self.state, (m1, m2, self.local), self.order_n,
+                    (t1, t2, np.ascontiguousarray(t3[:, self.z0:self.z1])))
+
+    def _launch(self, src, dst, off, zb, ze, flag, events):
+        m1, m2, _ = self.grid.cells_per_axis
+        h_mat, f1, f2, f3, cf = self._fac
+        plane = src[0].numel() * src.element_size()
+        stream = torch.cuda.current_stream()
+        e0 = torch.cuda.Event(enable_timing=True) if events is not None else None
+        if e0 is not None:
+            e0.record(stream)
+        rc = _native.lib().h3_fused_pass(
+            ctypes.c_void_p(src.data_ptr() + plane), ctypes.c_void_p(dst.data_ptr() + plane),
+            m1, m2, self.local, self.order_n, _ptr(h_mat), _ptr(f1), _ptr(f2), _ptr(f3), _ptr(cf),
+            self._q, off, zb, ze, 0, _native.VARIANTS[self.cfg.variant], ctypes.c_void_p(stream.cuda_stream),
+            ctypes.c_void_p(flag.data_ptr()), None)
+        _native.check(rc, "h3_fused_pass (slab)")
+        if e0 is not None:
+            e1 = torch.cuda.Event(enable_timing=True)
+            e1.record(stream)
+            events.append((e0, e1))
+
+    def half_step(self, src, dst, off, flag, timed=False):
+        works = exchange_halo(src, off, self.group, async_op=True)
+        ev = self.kernel_events if timed else None
+        L = self.local
+        # interior cell planes first (they do not read the ghost plane) ...
+        if off == 0:
+            self._launch(src, dst, off, 0, L - 1, flag, ev)
+        else:
+            self._launch(src, dst, off, 1, L, flag, ev)
+        for w in works:
+            w.wait()  # current stream waits for the NCCL stream
+        # ... then the boundary cell plane that does
+        if off == 0:
+            self._launch(src, dst, off, L - 1, L, flag, None)
+        else:
+            self._launch(src, dst, off, 0, 1, flag, None)
+
+    def step(self, timed=False) -> None:
+        self.half_step(self.bufs[0], self.bufs[1], 0, self.flags[0:1], timed)
+        self.half_step(self.bufs[1], self.bufs[0], -1, self.flags[1:2], timed)
+
+    def check(self, step_index=None) -> None:
+        host = self.flags.cpu().numpy()
+        for k, bad in enumerate(host):
+            if int(bad) != -1:
+                m1, m2, _ = self.grid.cells_per_axis
+                x, y, z = _node_of(int(bad), GridSpec((m1, m2, self.local)))
+                raise InstabilityError((x, y, z + self.z0), step_index)

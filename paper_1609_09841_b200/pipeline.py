@@ -1,0 +1,408 @@
+"""Grid time stepping on the B200: fused and two-pass half steps.
+
+Drop-in mirror of the reference's time-stepping API
+(pkg/src/hermite3d/pipeline.py): same names, signatures, argument meaning
+and errors (`StepConfig`, `OperatorSet`, `AllocationStats`,
+`InstabilityError`, `select_dt`, `half_step`, `full_step`, ...).  Underneath,
+every half step is one call into libh3b200.so (include/h3b200.h), issued on
+the caller's current torch CUDA stream; there is no CPU fallback.
+
+Differences that matter to callers:
+
+* `DofField` data lives on the GPU; `.data` is a host copy.
+* The finiteness check (pipeline.py:210-215) is fused into the kernels as a
+  device flag; `full_step` reads both half steps' flags back once, and the
+  second half step is skipped on the device when the first one failed, so
+  the observable state matches the reference's raise-after-first-half-step.
+* `StepConfig.variant` selects the kernel family: "separable" (exact
+  node-factorised evolution, HBM-bound; requires q >= 3(2N+1)), "literal"
+  (bit-identical to the reference), or "auto" (separable when exact,
+  literal otherwise; always literal for precision="single").
+* two_pass mode materialises the (2N+2)^3 coefficient field in slab chunks
+  along x3 when the whole field would not fit in free HBM; AllocationStats
+  records the buffer actually allocated.
+* `timings` accumulates CUDA-event seconds per kernel
+  ("monolithic" / "reconstruction" / "evolution").
+"""
+
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _native
+from .field import DofField, GridSpec
+from .operators import DerivOperator, InterpOperator, build_deriv_operator, build_interp_operator
+
+__all__ = [
+    "StepConfig", "CoeffField", "OperatorSet", "AllocationStats", "InstabilityError",
+    "select_dt", "tile_schedule", "half_step", "full_step", "run_steps", "resolve_tile_x1",
+    "set_worker_threads", "default_stages", "DEFAULT_TILE_X1", "MODES", "VARIANTS",
+]
+
+MODES = ("two_pass", "fused")
+VARIANTS = ("auto", "literal", "separable")
+ADVECTION_SPEED = 1.0
+
+# The reference's nominal per-kernel tile lengths (pipeline.py:52-56).  On the
+# GPU the tile is a launch hint only (results never depend on it); the value is
+# still validated exactly like the reference does.
+DEFAULT_TILE_X1 = {
+    "reconstruction": {1: 16, 2: 10, 3: 4},
+    "evolution": {1: 16, 2: 10, 3: 2},
+    "monolithic": {1: 12, 2: 10, 3: 2},
+}
+
+
+def default_stages(order_n: int, dims: int = 3) -> int:
+    """Stage count making local evolution exact: d(2N+1) (kernels.py:50-52)."""
+    return dims * (2 * order_n + 1)
+
+
+class InstabilityError(RuntimeError):
+    """Non-finite values appeared in a destination field (pipeline.py:59-66)."""
+
+    def __init__(self, node, step: int | None = None):
+        self.node = tuple(int(x) for x in node)
+        self.step = step
+        at = f" at step {step}" if step is not None else ""
+        super().__init__(f"non-finite values detected{at}, first offending node {self.node}")
+
+
+@dataclass(frozen=True)
+class StepConfig:
+    """Execution knobs for a half/full step (pipeline.py:69-90) plus `variant`."""
+
+    mode: str = "fused"
+    tile_x1: int | None = None
+    cfl: float = 0.9
+    stages_q: int | None = None
+    precision: str = "double"
+    variant: str = "auto"
+    coeff_budget_bytes: int | None = None
+
+    def __post_init__(self):
+        if self.mode not in MODES:
+            raise ValueError(f"mode must be one of {MODES}, got {self.mode!r}")
+        if self.tile_x1 is not None and self.tile_x1 < 1:
+            raise ValueError(f"tile_x1 must be >= 1, got {self.tile_x1}")
+        if not 0 < self.cfl <= 1:
+            raise ValueError(f"cfl must be in (0, 1], got {self.cfl}")
+        if self.stages_q is not None and self.stages_q < 1:
+            raise ValueError(f"stages_q must be >= 1, got {self.stages_q}")
+        if self.precision not in ("single", "double"):
+            raise ValueError(f"precision must be 'single' or 'double', got {self.precision!r}")
+        if self.variant not in VARIANTS:
+            raise ValueError(f"variant must be one of {VARIANTS}, got {self.variant!r}")
+
+    def stages(self, order_n: int) -> int:
+        return self.stages_q if self.stages_q is not None else default_stages(order_n)
+
+
+@dataclass
+class CoeffField:
+    """Grid-wide (or slab-chunk) reconstructed coefficients, two-pass intermediate."""
+
+    parity: str
+    data: torch.Tensor
+    z_begin: int = 0
+    z_end: int = 0
+
+
+@dataclass(frozen=True)
+class OperatorSet:
+    """Immutable per-(N, grid) operator bundle (pipeline.py:101-128)."""
+
+    order_n: int
+    interp: InterpOperator
+    derivs: tuple[DerivOperator, DerivOperator, DerivOperator]
+
+    @classmethod
+    def for_grid(cls, grid: GridSpec, order_n: int) -> "OperatorSet":
+        h1, h2, h3 = grid.spacings
+        return cls(order_n=order_n, interp=build_interp_operator(order_n),
+                   derivs=(build_deriv_operator(order_n, h1), build_deriv_operator(order_n, h2),
+                           build_deriv_operator(order_n, h3)))
+
+    @property
+    def interp_triple(self):
+        return (self.interp, self.interp, self.interp)
+
+    @property
+    def side(self) -> int:
+        return 2 * self.order_n + 2
+
+
+class AllocationStats:
+    """Grid-sized auxiliary allocations made by the pipeline (pipeline.py:131-152)."""
+
+    def __init__(self):
+        self.events: list[tuple[str, int]] = []
+        self._live: dict[str, int] = {}
+        self.live_bytes = 0
+        self.peak_aux_bytes = 0
+
+    def allocate(self, name: str, nbytes: int) -> None:
+        self.events.append((name, nbytes))
+        self._live[name] = nbytes
+        self.live_bytes += nbytes
+        self.peak_aux_bytes = max(self.peak_aux_bytes, self.live_bytes)
+
+    def release(self, name: str) -> None:
+        self.live_bytes -= self._live.pop(name, 0)
+
+
+def select_dt(grid: GridSpec, cfg: StepConfig) -> float:
+    """dt = cfl * min_k h_k / speed (pipeline.py:155-163)."""
+    if not 0 < cfg.cfl <= 1:
+        raise ValueError(f"cfl must be in (0, 1], got {cfg.cfl}")
+    return cfg.cfl * min(grid.spacings) / ADVECTION_SPEED
+
+
+def resolve_tile_x1(kernel: str, order_n: int, m1: int, override: int | None = None) -> int:
+    """Tile length: explicit override (validated), else the nominal default (pipeline.py:166-173)."""
+    if override is not None:
+        if not 1 <= override <= m1:
+            raise ValueError(f"tile_x1 must be in [1, {m1}], got {override}")
+        return override
+    table = DEFAULT_TILE_X1.get(kernel, DEFAULT_TILE_X1["monolithic"])
+    return max(1, min(m1, table.get(order_n, 4)))
+
+
+def tile_schedule(grid: GridSpec, tile_x1: int) -> np.ndarray:
+    """The reference's tile table [c3, c2, x1_start, x1_len] (pipeline.py:176-186).
+
+    Kept for API compatibility (and built vectorised); the CUDA kernels use
+    their own launch geometry, which partitions the same cells.
+    """
+    m1, m2, m3 = grid.cells_per_axis
+    if not 1 <= tile_x1 <= m1:
+        raise ValueError(f"tile_x1 must be in [1, {m1}], got {tile_x1}")
+    starts = np.arange(0, m1, tile_x1, dtype=np.int64)
+    lens = np.minimum(tile_x1, m1 - starts)
+    c3, c2, k = np.meshgrid(np.arange(m3), np.arange(m2), np.arange(len(starts)), indexing="ij")
+    return np.stack([c3.ravel(), c2.ravel(), starts[k.ravel()], lens[k.ravel()]], axis=1).astype(np.int64)
+
+
+def set_worker_threads(n: int | None) -> int:
+    """GPU analogue of the worker-pool size (pipeline.py:189-194): returns the SM count."""
+    return torch.cuda.get_device_properties(torch.cuda.current_device()).multi_processor_count
+
+
+def _factor_arrays(ops: OperatorSet, dtype, delta: float, q: int):
+    """Kernel scale factors, pre-cast to the field dtype (pipeline.py:197-207)."""
+    s = ops.side
+    h_mat = np.ascontiguousarray(ops.interp.matrix.astype(dtype))
+    facs = []
+    for d in ops.derivs:
+        fac = np.zeros(s, dtype=dtype)
+        fac[:-1] = (np.arange(1, s) * (1.0 / d.spacing)).astype(dtype)
+        facs.append(fac)
+    cfac = np.asarray([delta / k for k in range(1, q + 1)], dtype=dtype)
+    return h_mat, facs[0], facs[1], facs[2], cfac
+
+
+def _ptr(a: np.ndarray):
+    return a.ctypes.data_as(ctypes.c_void_p)
+
+
+def _new_flags(count: int, device) -> torch.Tensor:
+    return torch.full((count,), -1, dtype=torch.int64, device=device)  # == H3_NO_BAD_NODE
+
+
+def _node_of(lin: int, grid: GridSpec) -> tuple[int, int, int]:
+    m1, m2, _ = grid.cells_per_axis
+    lin = int(lin) & 0xFFFFFFFFFFFFFFFF
+    return (lin % m1, (lin // m1) % m2, lin // (m1 * m2))
+
+
+def _variant_code(cfg: StepConfig, precision: str) -> int:
+    if precision == "single" and cfg.variant == "separable":
+        raise ValueError("the separable variant is FP64-only; use variant='literal' or 'auto'")
+    return _native.VARIANTS[cfg.variant]
+
+
+def _coeff_chunk_planes(grid: GridSpec, order_n: int, itemsize: int, budget: int | None) -> int:
+    m1, m2, m3 = grid.cells_per_axis
+    s = 2 * order_n + 2
+    per_plane = m1 * m2 * s ** 3 * itemsize
+    if budget is None:
+        free, _total = torch.cuda.mem_get_info()
+        budget = max(per_plane, int(0.85 * free) - (1 << 30))
+    return max(1, min(m3, budget // per_plane))
+
+
+def half_step(
+    src: DofField,
+    dst: DofField,
+    cfg: StepConfig,
+    ops: OperatorSet,
+    stats: AllocationStats | None = None,
+    dt: float | None = None,
+    step_index: int | None = None,
+    timings: dict | None = None,
+    *,
+    _flag: torch.Tensor | None = None,
+    _guard: torch.Tensor | None = None,
+    _check: bool = True,
+) -> None:
+    """Advance src's DOFs by dt/2 onto the opposite-parity field dst (pipeline.py:218-274)."""
+    if src.grid.parity == dst.grid.parity:
+        raise ValueError(f"src and dst must have opposite parity, both are {src.grid.parity!r}")
+    if src.tensor.data_ptr() == dst.tensor.data_ptr():
+        raise ValueError("src and dst must be disjoint fields")
+    if src.grid.cells_per_axis != dst.grid.cells_per_axis or src.order_n != dst.order_n:
+        raise ValueError("src and dst must share grid dimensions and order")
+    if src.tensor.dtype != dst.tensor.dtype or src.device != dst.device:
+        raise ValueError("src and dst must share dtype and device")
+    if dt is None:
+        dt = select_dt(src.grid, cfg)
+    order_n = ops.order_n
+    q = cfg.stages(order_n)
+    delta = dt / 2
+    off = 0 if src.grid.parity == "primary" else -1
+    kernel = "monolithic" if cfg.mode == "fused" else "reconstruction"
+    resolve_tile_x1(kernel, order_n, src.grid.cells_per_axis[0], cfg.tile_x1)
+    precision = src.precision
+    dtype = np.float64 if precision == "double" else np.float32
+    h_mat, fac1, fac2, fac3, cfac = _factor_arrays(ops, dtype, delta, q)
+    variant = _variant_code(cfg, precision)
+
+    lib = _native.lib()
+    m1, m2, m3 = src.grid.cells_per_axis
+    device = src.device
+    with torch.cuda.device(device):
+        stream = torch.cuda.current_stream(device)
+        sh = ctypes.c_void_p(stream.cuda_stream)
+        flag = _flag if _flag is not None else _new_flags(1, device)
+        fptr = ctypes.c_void_p(flag.data_ptr())
+        gptr = ctypes.c_void_p(_guard.data_ptr()) if _guard is not None else None
+        events = []
+
+        def mark():
+            if timings is not None:
+                ev = torch.cuda.Event(enable_timing=True)
+                ev.record(stream)
+                events.append(ev)
+
+        if cfg.mode == "fused":
+            fn = lib.h3_fused_pass if precision == "double" else lib.h3_fused_pass_f32
+            mark()
+            rc = fn(ctypes.c_void_p(src.tensor.data_ptr()), ctypes.c_void_p(dst.tensor.data_ptr()),
+                    m1, m2, m3, order_n, _ptr(h_mat), _ptr(fac1), _ptr(fac2), _ptr(fac3), _ptr(cfac),
+                    q, off, 0, m3, 1, variant, sh, fptr, gptr)
+            _native.check(rc, "h3_fused_pass")
+            mark()
+            if timings is not None:
+                events[1].synchronize()
+                timings["monolithic"] = timings.get("monolithic", 0.0) + events[0].elapsed_time(events[1]) / 1e3
+        else:
+            s = ops.side
+            chunk = _coeff_chunk_planes(src.grid, order_n, src.tensor.element_size(), cfg.coeff_budget_bytes)
+            coeff = torch.empty((chunk, m2, m1, s, s, s), dtype=src.tensor.dtype, device=device)
+            if stats is not None:
+                stats.allocate("coeff_field", coeff.numel() * coeff.element_size())
+            try:
+                recon = lib.h3_recon_pass if precision == "double" else lib.h3_recon_pass_f32
+                evolve = lib.h3_evolve_pass if precision == "double" else lib.h3_evolve_pass_f32
+                cptr = ctypes.c_void_p(coeff.data_ptr())
+                t_rec = t_evo = 0.0
+                for z0 in range(0, m3, chunk):
+                    z1 = min(m3, z0 + chunk)
+                    events.clear()
+                    mark()
+                    rc = recon(ctypes.c_void_p(src.tensor.data_ptr()), cptr, m1, m2, m3, order_n,
+                               _ptr(h_mat), off, z0, z1, 1, variant, sh, gptr)
+                    _native.check(rc, "h3_recon_pass")
+                    mark()
+                    rc = evolve(cptr, ctypes.c_void_p(dst.tensor.data_ptr()), m1, m2, m3, order_n,
+                                _ptr(fac1), _ptr(fac2), _ptr(fac3), _ptr(cfac), q, z0, z1, variant,
+                                sh, fptr, gptr)
+                    _native.check(rc, "h3_evolve_pass")
+                    mark()
+                    if timings is not None:
+                        events[2].synchronize()
+                        t_rec += events[0].elapsed_time(events[1]) / 1e3
+                        t_evo += events[1].elapsed_time(events[2]) / 1e3
+                if timings is not None:
+                    timings["reconstruction"] = timings.get("reconstruction", 0.0) + t_rec
+                    timings["evolution"] = timings.get("evolution", 0.0) + t_evo
+            finally:
+                if stats is not None:
+                    stats.release("coeff_field")
+                # the caching allocator reuses the block only after queued kernels finish
+                coeff.record_stream(stream)
+                del coeff
+        if _check:
+            bad = int(flag[0].item())
+            if bad != -1:
+                raise InstabilityError(node=_node_of(bad, dst.grid), step=step_index)
+
+
+def full_step(
+    state: DofField,
+    scratch: DofField,
+    cfg: StepConfig,
+    ops: OperatorSet,
+    stats: AllocationStats | None = None,
+    dt: float | None = None,
+    step_index: int | None = None,
+    timings: dict | None = None,
+) -> None:
+    """One full dt: primary -> dual -> primary, state updated in place (pipeline.py:277-293)."""
+    if state.grid.parity != "primary" or scratch.grid.parity != "dual":
+        raise ValueError("full_step expects state on the primary grid and scratch on the dual grid")
+    if dt is None:
+        dt = select_dt(state.grid, cfg)
+    flags = _new_flags(2, state.device)
+    half_step(state, scratch, cfg, ops, stats=stats, dt=dt, step_index=step_index, timings=timings,
+              _flag=flags[0:1], _check=False)
+    half_step(scratch, state, cfg, ops, stats=stats, dt=dt, step_index=step_index, timings=timings,
+              _flag=flags[1:2], _guard=flags[0:1], _check=False)
+    _raise_first_bad(flags.cpu().numpy(), (scratch.grid, state.grid), [step_index, step_index])
+
+
+def _raise_first_bad(host_flags, grids, steps) -> None:
+    for k, bad in enumerate(host_flags):
+        if int(bad) != -1:
+            raise InstabilityError(node=_node_of(int(bad), grids[k % 2]), step=steps[k])
+
+
+def run_steps(
+    state: DofField,
+    scratch: DofField,
+    cfg: StepConfig,
+    ops: OperatorSet,
+    steps: int,
+    dt: float | None = None,
+    first_step: int = 0,
+    stats: AllocationStats | None = None,
+) -> None:
+    """`steps` full steps with ONE host synchronisation at the end.
+
+    Every half step is guarded on the device by its predecessor's flag, so
+    after an instability nothing further is computed, and the error raised
+    names the same half step and node the per-step loop of the reference
+    (runner.py:160-168) would have reported.
+    """
+    if state.grid.parity != "primary" or scratch.grid.parity != "dual":
+        raise ValueError("run_steps expects state on the primary grid and scratch on the dual grid")
+    if steps <= 0:
+        return
+    if dt is None:
+        dt = select_dt(state.grid, cfg)
+    flags = _new_flags(2 * steps, state.device)
+    prev = None
+    for k in range(steps):
+        f0, f1 = flags[2 * k:2 * k + 1], flags[2 * k + 1:2 * k + 2]
+        half_step(state, scratch, cfg, ops, stats=stats, dt=dt, step_index=first_step + k,
+                  _flag=f0, _guard=prev, _check=False)
+        half_step(scratch, state, cfg, ops, stats=stats, dt=dt, step_index=first_step + k,
+                  _flag=f1, _guard=f0, _check=False)
+        prev = f1
+    host = flags.cpu().numpy()
+    _raise_first_bad(host, (scratch.grid, state.grid),
+                     [first_step + k // 2 for k in range(2 * steps)])

@@ -1,0 +1,58 @@
+"""Convergence order and long-run stability of the GPU path against the exact plane wave.
+
+Mirrors SPEC.md acceptance criteria 1 and 6 (reference SPEC.md:462, 467) and the
+runner's step planning (reference runner.py:65-76): dt shrinks so an integer
+number of steps lands exactly on the final time.
+"""
+
+import math
+
+import pytest
+
+import paper_1609_09841_b200 as hb
+
+pytestmark = pytest.mark.gpu
+
+
+def solve(order_n, m, final_time, variant, mode="fused", wavenumber=1):
+    grid = hb.GridSpec((m, m, m))
+    cfg = hb.StepConfig(mode=mode, variant=variant)
+    ops = hb.OperatorSet.for_grid(grid, order_n)
+    dt_max = hb.select_dt(grid, cfg)
+    steps = max(1, math.ceil(final_time / dt_max - 1e-12))
+    dt = final_time / steps
+    ic = hb.plane_wave(wavenumber)
+    state = hb.init_field(ic, grid, order_n)
+    scratch = hb.DofField.zeros(grid.with_parity("dual"), order_n)
+    hb.run_steps(state, scratch, cfg, ops, steps, dt=dt)
+    return hb.compute_error(state, hb.exact_solution(ic, steps * dt))
+
+
+@pytest.mark.parametrize("variant", ["literal", "separable"])
+@pytest.mark.parametrize("order_n,levels", [(1, (8, 16, 32)), (2, (8, 16)), (3, (6, 12))])
+def test_convergence_order(order_n, levels, variant):
+    errs = [solve(order_n, m, 0.25, variant).l_inf for m in levels]
+    order = math.log2(errs[-2] / errs[-1]) / math.log2(levels[-1] / levels[-2])
+    assert order >= 2 * order_n + 0.5, (errs, order)
+
+
+@pytest.mark.parametrize("mode", ["fused", "two_pass"])
+def test_convergence_order_m5_high_wavenumber(mode):
+    """m=5 (config 4 of BASELINE.json) with k chosen so the coarse grid is resolved but
+    not at the FP64 floor: expected order >= 2N + 0.5 = 10.5."""
+    errs = [solve(5, m, 0.1, "separable", mode, wavenumber=4).l_inf for m in (16, 24)]
+    order = math.log2(errs[0] / errs[1]) / math.log2(24 / 16)
+    assert order >= 10.5, (errs, order)
+
+
+@pytest.mark.parametrize("order_n", [1, 2, 3])
+def test_stability_500_steps(order_n):
+    """SPEC acceptance 6: cfl 0.9, 500 steps, unit single mode, 16^3: L_inf <= 1.05."""
+    grid = hb.GridSpec((16, 16, 16))
+    cfg = hb.StepConfig()
+    ops = hb.OperatorSet.for_grid(grid, order_n)
+    ic = hb.SeparableIC(((hb.FourierMode(1.0, 1, 0.0), hb.Constant(1.0), hb.Constant(1.0)),))
+    state = hb.init_field(ic, grid, order_n)
+    scratch = hb.DofField.zeros(grid.with_parity("dual"), order_n)
+    hb.run_steps(state, scratch, cfg, ops, 500)
+    assert float(abs(state.tensor[..., 0, 0, 0]).max()) <= 1.05
