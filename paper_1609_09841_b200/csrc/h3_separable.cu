@@ -26,37 +26,60 @@
 namespace h3 {
 
 template <int N> struct SepTile;
-// TX, TY: cells per CTA; PAD: doubles of padding per node block in smem.
-template <> struct SepTile<0> { static constexpr int TX = 32, TY = 8, PAD = 1; };
-template <> struct SepTile<1> { static constexpr int TX = 16, TY = 8, PAD = 2; };
-template <> struct SepTile<2> { static constexpr int TX = 8, TY = 8, PAD = 1; };
-template <> struct SepTile<3> { static constexpr int TX = 8, TY = 8, PAD = 4; };
-template <> struct SepTile<4> { static constexpr int TX = 8, TY = 4, PAD = 1; };
-template <> struct SepTile<5> { static constexpr int TX = 8, TY = 4, PAD = 2; };
+// TX, TY: cells per CTA.  Shared-memory layouts (doubles), chosen by
+// tools/smem_layout_search.py so that every hot shared access of the kernel is
+// bank-conflict free (or as close as the tile allows):
+//   U node [j3][j2][j1]: j3 stride UJ, node stride UNS  (staged input plane)
+//   W node [j3][m1][j2]: j3 stride WJ, node stride WNS  (pass-x1 output)
+template <> struct SepTile<0> { static constexpr int TX = 32, TY = 8, UJ = 1, UNS = 1, WJ = 1, WNS = 1; };
+template <> struct SepTile<1> { static constexpr int TX = 16, TY = 8, UJ = 4, UNS = 8, WJ = 6, WNS = 12; };
+template <> struct SepTile<2> { static constexpr int TX = 8, TY = 8, UJ = 9, UNS = 27, WJ = 12, WNS = 41; };
+template <> struct SepTile<3> { static constexpr int TX = 8, TY = 8, UJ = 18, UNS = 72, WJ = 20, WNS = 82; };
+template <> struct SepTile<4> { static constexpr int TX = 8, TY = 4, UJ = 25, UNS = 125, WJ = 27, WNS = 137; };
+template <> struct SepTile<5> { static constexpr int TX = 8, TY = 4, UJ = 36, UNS = 216, WJ = 38, WNS = 228; };
 
-template <int N, int TX, int TY, int PAD>
+template <int N>
 struct SepGeom {
+    using L = SepTile<N>;
+    static constexpr int TX = L::TX, TY = L::TY;
     static constexpr int n = N + 1, n2 = n * n, n3 = n2 * n;
     static constexpr int NX = TX + 1, NY = TY + 1;
-    static constexpr int NS = n3 + PAD;                 // node stride in smem (doubles)
+    static constexpr int UJ = L::UJ, UNS = L::UNS, WJ = L::WJ, WNS = L::WNS;
     static constexpr int THREADS = TX * TY * n;
-    static constexpr int VEC = (n3 % 2 == 0 && NS % 2 == 0) ? 2 : 1;  // doubles per cp.async
-    static constexpr int CPN = n3 / VEC;                 // copies per node
+    static constexpr int VEC = (n % 2 == 0) ? 2 : 1;    // doubles per shared vector access
+    static constexpr int FVEC = (n3 % 2 == 0 && UJ % 2 == 0 && UNS % 2 == 0 && n2 % 2 == 0) ? 2 : 1;
+    static constexpr int CPN = n3 / FVEC;                 // cp.async pieces per node
     static constexpr int NCOPY = NY * NX * CPN;
     static constexpr int L1 = NY * TX * n2;              // pass-x1 lines
     static constexpr int R1 = (L1 + THREADS - 1) / THREADS;
-    static constexpr size_t U_DOUBLES = (size_t)NY * NX * NS;
-    static constexpr size_t W_DOUBLES = (size_t)NY * TX * NS;
-    static constexpr size_t SMEM = (2 * U_DOUBLES + W_DOUBLES) * sizeof(double);
+    static constexpr size_t U_DOUBLES = (size_t)NY * NX * UNS;
+    static constexpr size_t W_DOUBLES = (size_t)NY * TX * WNS;
+    static constexpr size_t SMEM = (2 * U_DOUBLES + W_DOUBLES) * sizeof(double) + NY * NX * sizeof(int);
 };
 
-template <int N, int TX, int TY, int PAD>
-__global__ void __launch_bounds__(SepGeom<N, TX, TY, PAD>::THREADS)
+template <int CNT, int VEC>
+__device__ __forceinline__ void lds_vec(double (&dst)[CNT], const double* src) {
+    if constexpr (VEC == 2) {
+#pragma unroll
+        for (int j = 0; j < CNT; j += 2) {
+            const double2 v = *reinterpret_cast<const double2*>(src + j);
+            dst[j] = v.x;
+            dst[j + 1] = v.y;
+        }
+    } else {
+#pragma unroll
+        for (int j = 0; j < CNT; ++j) dst[j] = src[j];
+    }
+}
+
+template <int N>
+__global__ void __launch_bounds__(SepGeom<N>::THREADS)
 sep_fused_kernel(const double* __restrict__ src, double* __restrict__ dst, Dims d, int off,
                  int zchunk, const __grid_constant__ SepOps<N> p,
                  unsigned long long* first_bad, const unsigned long long* guard) {
-    using G = SepGeom<N, TX, TY, PAD>;
-    constexpr int n = G::n, n2 = G::n2, n3 = G::n3, NX = G::NX, NS = G::NS;
+    using G = SepGeom<N>;
+    constexpr int TX = G::TX, n = G::n, n2 = G::n2, n3 = G::n3, NX = G::NX;
+    constexpr int UJ = G::UJ, UNS = G::UNS, WJ = G::WJ, WNS = G::WNS;
     if (guarded_out(guard, first_bad)) return;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     double* U0 = reinterpret_cast<double*>(smem_raw);
@@ -65,26 +88,48 @@ sep_fused_kernel(const double* __restrict__ src, double* __restrict__ dst, Dims 
 
     const int tid = threadIdx.x;
     const int M1 = (int)d.M1, M2 = (int)d.M2;
-    const int cx0 = blockIdx.x * TX, cy0 = blockIdx.y * TY;
+    const int cx0 = blockIdx.x * TX, cy0 = blockIdx.y * G::TY;
     const int64_t zc0 = d.z_begin + (int64_t)blockIdx.z * zchunk;
     const int64_t zc1 = min(zc0 + (int64_t)zchunk, d.z_end);
     const int P = (int)(zc1 - zc0) + 1;  // node planes touched by this chunk
     const int64_t plane_elems = (int64_t)M1 * M2 * n3;
 
+    // Global offset (doubles, relative to the plane base) of every tile node: the
+    // periodic wrap is resolved once per CTA, so the per-plane copy loop is just
+    // table lookup + LDGSTS.
+    int* nodeoff = reinterpret_cast<int*>(W + G::W_DOUBLES);
+    for (int node = tid; node < G::NY * NX; node += G::THREADS) {
+        const int ly = node / NX, lx = node - (node / NX) * NX;
+        int gx = cx0 + off + lx, gy = cy0 + off + ly;
+        gx %= M1; if (gx < 0) gx += M1;
+        gy %= M2; if (gy < 0) gy += M2;
+        nodeoff[node] = (gy * M1 + gx) * n3;
+    }
+    __syncthreads();
+
     auto issue = [&](int pl, double* Ub) {
         const int64_t gz = zplane(zc0 + off + pl, d.M3, d.periodic_z);
         const double* base = src + gz * plane_elems;
-        for (int e = tid; e < G::NCOPY; e += G::THREADS) {
-            const int ly = e / (NX * G::CPN);
-            const int r = e - ly * (NX * G::CPN);
-            const int lx = r / G::CPN;
-            const int pc = r - lx * G::CPN;
-            int gx = cx0 + off + lx, gy = cy0 + off + ly;
-            if (gx < 0) gx += M1; else if (gx >= M1) gx %= M1;
-            if (gy < 0) gy += M2; else if (gy >= M2) gy %= M2;
-            const double* g = base + ((int64_t)gy * M1 + gx) * n3 + pc * G::VEC;
-            double* s = Ub + (ly * NX + lx) * NS + pc * G::VEC;
-            if (G::VEC == 2) cp_async16(s, g); else cp_async8(s, g);
+        if constexpr (G::THREADS % G::CPN == 0) {
+            // each thread always copies the same piece of successive nodes
+            constexpr int STEP = G::THREADS / G::CPN;
+            const int pc = tid % G::CPN;
+            const int dbl = pc * G::FVEC;
+            const int soff = (dbl / n2) * UJ + dbl % n2;
+#pragma unroll 4
+            for (int node = tid / G::CPN; node < G::NY * NX; node += STEP) {
+                const double* g = base + nodeoff[node] + dbl;
+                double* sp = Ub + node * UNS + soff;
+                if (G::FVEC == 2) cp_async16(sp, g); else cp_async8(sp, g);
+            }
+        } else {
+            for (int e = tid; e < G::NCOPY; e += G::THREADS) {
+                const int node = e / G::CPN;
+                const int dbl = (e - node * G::CPN) * G::FVEC;
+                const double* g = base + nodeoff[node] + dbl;
+                double* sp = Ub + node * UNS + (dbl / n2) * UJ + dbl % n2;
+                if (G::FVEC == 2) cp_async16(sp, g); else cp_async8(sp, g);
+            }
         }
     };
 
@@ -104,26 +149,26 @@ sep_fused_kernel(const double* __restrict__ src, double* __restrict__ dst, Dims 
     issue(0, U0);
     cp_async_commit();
     for (int pl = 0; pl < P; ++pl) {
-        double* Ub = (pl & 1) ? U1 : U0;
+        const double* Ub = (pl & 1) ? U1 : U0;
         if (pl + 1 < P) issue(pl + 1, (pl & 1) ? U0 : U1);
         cp_async_commit();
         cp_async_wait<1>();
         __syncthreads();
 
-        // ---- pass x1: W[ly][ix][j3][j2][m1] -------------------------------------------
+        // ---- pass x1: W[ly][ix][j3][m1][j2] = A1^0 U[ly][ix] + A1^1 U[ly][ix+1] ------------
 #pragma unroll
         for (int r = 0; r < G::R1; ++r) {
             const int l = tid + r * G::THREADS;
-            if (l < G::L1) {
+            if (G::L1 % G::THREADS == 0 || l < G::L1) {
                 const int j32 = l % n2;
                 const int rest = l / n2;
                 const int lix = rest % TX, ly = rest / TX;
-                const double* u0 = Ub + (ly * NX + lix) * NS + j32 * n;
-                const double* u1 = u0 + NS;
+                const int j3 = j32 / n, j2 = j32 - (j32 / n) * n;
+                const double* u0 = Ub + (ly * NX + lix) * UNS + j3 * UJ + j2 * n;
                 double a[n], b[n];
-#pragma unroll
-                for (int j = 0; j < n; ++j) { a[j] = u0[j]; b[j] = u1[j]; }
-                double* wout = W + (ly * TX + lix) * NS + j32 * n;
+                lds_vec<n, G::VEC>(a, u0);
+                lds_vec<n, G::VEC>(b, u0 + UNS);
+                double* wout = W + (ly * TX + lix) * WNS + j3 * WJ + j2;
 #pragma unroll
                 for (int m = 0; m < n; ++m) {
                     double acc = p.A[0][m][0] * a[0];
@@ -131,7 +176,7 @@ sep_fused_kernel(const double* __restrict__ src, double* __restrict__ dst, Dims 
                     for (int j = 1; j < n; ++j) acc = fma(p.A[0][m][j], a[j], acc);
 #pragma unroll
                     for (int j = 0; j < n; ++j) acc = fma(p.A[0][m][n + j], b[j], acc);
-                    wout[m] = acc;
+                    wout[m * n] = acc;
                 }
             }
         }
@@ -139,14 +184,14 @@ sep_fused_kernel(const double* __restrict__ src, double* __restrict__ dst, Dims 
 
         // ---- pass x2 + x3 ----------------------------------------------------------------
         {
-            const double* w0 = W + (iy * TX + ix) * NS + m1;
-            const double* w1 = w0 + TX * NS;
+            const double* w0 = W + (iy * TX + ix) * WNS + m1 * n;
+            const double* w1 = w0 + TX * WNS;
             double accN[n][n];
 #pragma unroll
             for (int j3 = 0; j3 < n; ++j3) {
                 double a[n], b[n];
-#pragma unroll
-                for (int j = 0; j < n; ++j) { a[j] = w0[(j3 * n + j) * n]; b[j] = w1[(j3 * n + j) * n]; }
+                lds_vec<n, G::VEC>(a, w0 + j3 * WJ);
+                lds_vec<n, G::VEC>(b, w1 + j3 * WJ);
                 double v[n];
 #pragma unroll
                 for (int m = 0; m < n; ++m) {
@@ -193,10 +238,10 @@ template <int N>
 static int sep_fused_n(const double* src, double* dst, const Dims& d, const double* A, int off,
                        cudaStream_t st, unsigned long long* first_bad,
                        const unsigned long long* guard) {
-    using T = SepTile<N>;
-    using G = SepGeom<N, T::TX, T::TY, T::PAD>;
+    using G = SepGeom<N>;
     const int64_t nz = d.z_end - d.z_begin;
     if (nz <= 0 || d.M1 <= 0 || d.M2 <= 0) return 0;
+    if (d.M1 * d.M2 * G::n3 >= (int64_t(1) << 31)) return (int)cudaErrorInvalidValue;  // int32 plane offsets
     SepOps<N> ops;
     for (int k = 0; k < 3; ++k)
         for (int m = 0; m < G::n; ++m)
@@ -204,13 +249,13 @@ static int sep_fused_n(const double* src, double* dst, const Dims& d, const doub
                 ops.A[k][m][c] = A[(k * G::n + m) * 2 * G::n + c];
                 ops.Sh[k][m][c] = 0.0;
             }
-    auto kern = sep_fused_kernel<N, T::TX, T::TY, T::PAD>;
+    auto kern = sep_fused_kernel<N>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)G::SMEM);
     if (e != cudaSuccess) return (int)e;
     int per_sm = 0;
     e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, G::THREADS, G::SMEM);
     if (e != cudaSuccess) return (int)e;
-    const int64_t gx = (d.M1 + T::TX - 1) / T::TX, gy = (d.M2 + T::TY - 1) / T::TY;
+    const int64_t gx = (d.M1 + G::TX - 1) / G::TX, gy = (d.M2 + G::TY - 1) / G::TY;
     // enough CTAs for ~4 waves; split the z march only when the x-y tiling is too coarse
     const int64_t want = (int64_t)num_sms() * (per_sm > 0 ? per_sm : 1) * 4;
     int64_t zsplit = (want + gx * gy - 1) / (gx * gy);
