@@ -1,0 +1,344 @@
+// FP64 tensor-core (DMMA m8n8k4) fused half step for order N = 3 (n = 4).
+//
+// Same algorithm as sep_fused_kernel (h3_separable.cu): the exact separable local
+// evolution out(c) = sum_a (A3^a3 (x) A2^a2 (x) A1^a1) u(c + off + a), applied as
+// three node-factorised 1-D passes.  Each pass is a batch of tiny GEMMs
+//     D[line][col] = sum_k data[line][k] * B[k][col]        (8 lines x 4 k x 8 cols)
+// issued as mma.sync.m8n8k4.f64: one instruction does 256 FMAs, so the FP64 work
+// costs 1/8 of the issue slots of DFMA and the operator never leaves registers
+// (each lane holds one B element per operator).  B200's FP64 tensor rate equals its
+// FP64 FMA rate (measured 37 TFLOP/s for both, tools/micro), so this is about issue
+// efficiency, not peak flops.
+//
+// n = 4 outputs per line fill only half of the 8 columns, so the columns carry both
+// roles of a node: its contribution to the cell on its right (A^0) and on its left
+// (A^1).  Walking along an axis, consecutive nodes alternate the column order, so the
+// two contributions to one cell land in the SAME lanes and are summed by the MMA's
+// own accumulator -- no shuffles:
+//     node parity 0: cols 0-3 = A^0 (cell p, pending)   cols 4-7 = A^1 (cell p-1, completes)
+//     node parity 1: cols 0-3 = A^1 (cell p-1, completes) cols 4-7 = A^0 (cell p, pending)
+// After each MMA the completed half of the lanes is stored and zeroed.
+//
+// CTA: 8 x 7 cells in (x1, x2), 16 warps, marching along x3 ("register rolling" in
+// x3).  Per node plane:
+//   x1: warp (row ly, line-half h) walks the 9 nodes of its row        (9 MMAs)
+//   x2: warp (column ix, line-half h) walks the 8 rows of its column    (8 MMAs)
+//   x3: warp owns 7 (cell, line-half) chains across planes             (7 MMAs)
+// Input planes stream in with cp.async (3 stages); the pass results are exchanged
+// through bank-conflict-free shared-memory layouts.
+#include <cstdlib>
+
+#include "h3_launch.h"
+
+namespace h3 {
+
+__device__ __forceinline__ void dmma884(double& d0, double& d1, double a, double b) {
+    asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+        : "+d"(d0), "+d"(d1)
+        : "d"(a), "d"(b));
+}
+
+// Tile / pipeline configuration of the DMMA kernel.
+template <int TY_, int WARPS_, int STAGES_, bool VALIAS_, int MINB_ = 1>
+struct Dm3Cfg {
+    static constexpr int MINB = MINB_;  // CTAs per SM the register budget is sized for
+    static constexpr int n = 4, n3 = 64;
+    static constexpr int TX = 8, TY = TY_, NX = TX + 1, NY = TY + 1, NCOL = NX * NY;
+    static constexpr int WARPS = WARPS_, THREADS = 32 * WARPS, STAGES = STAGES_;
+    static constexpr bool VALIAS = VALIAS_;  // x2 output reuses the consumed input stage
+    static constexpr int UNS = 64;            // U node stride (dense [j3][j2][j1])
+    static constexpr int WRS = 20, WCS = 80;  // W  [j3][m1][j2]: j3-row stride, cell stride
+    static constexpr int VRS = 17, VCS = 68;  // V  [m2][m1][j3]: m2-row stride, cell stride
+    static constexpr int T1 = 2 * NY, K1 = (T1 + WARPS - 1) / WARPS;  // x1 (row, half) tasks
+    static constexpr int T2 = 2 * TX, K2 = (T2 + WARPS - 1) / WARPS;  // x2 (column, half) tasks
+    static constexpr int T3 = 2 * TX * TY, K3 = T3 / WARPS;           // x3 (cell, half) chains
+    static constexpr int CPW = (NCOL + WARPS - 1) / WARPS;            // node copies per warp
+    static constexpr size_t U_D = (size_t)NCOL * UNS;
+    static constexpr size_t W_D = (size_t)NY * TX * WCS;
+    static constexpr size_t V_D = (size_t)TY * TX * VCS;
+    static constexpr size_t SMEM = (STAGES * U_D + W_D + (VALIAS ? 0 : V_D)) * sizeof(double);
+    static_assert(T3 % WARPS == 0, "x3 chains must divide evenly among warps");
+    static_assert(!VALIAS || V_D <= U_D, "aliased V must fit in one input stage");
+    static_assert(STAGES >= 2, "need at least double buffering");
+};
+
+template <class C>
+__global__ void __launch_bounds__(C::THREADS, C::MINB)
+sep_fused_dmma3_kernel(const double* __restrict__ src, double* __restrict__ dst, Dims d, int off,
+                       int zchunk, const __grid_constant__ SepOps<3> p,
+                       unsigned long long* first_bad, const unsigned long long* guard) {
+    constexpr int n = C::n, n3 = C::n3, TX = C::TX, TY = C::TY, NX = C::NX, NY = C::NY;
+    constexpr int NCOL = C::NCOL, WARPS = C::WARPS, STAGES = C::STAGES, UNS = C::UNS;
+    constexpr int WRS = C::WRS, WCS = C::WCS, VRS = C::VRS, VCS = C::VCS;
+    constexpr int K1 = C::K1, K2 = C::K2, K3 = C::K3;
+    if (guarded_out(guard, first_bad)) return;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    double* U = reinterpret_cast<double*>(smem_raw);
+    double* W = U + STAGES * C::U_D;
+    double* Vfix = W + C::W_D;
+
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int q = lane & 3, g = lane >> 2, par = q >> 1;  // fragment coordinates
+    const int M1 = (int)d.M1, M2 = (int)d.M2;
+    const int cx0 = blockIdx.x * TX, cy0 = blockIdx.y * TY;
+    const int64_t zc0 = d.z_begin + (int64_t)blockIdx.z * zchunk;
+    const int64_t zc1 = min(zc0 + (int64_t)zchunk, d.z_end);
+    const int P = (int)(zc1 - zc0) + 1;
+    const int64_t plane_elems = (int64_t)M1 * M2 * n3;
+
+    // operator fragments: lane holds B[k = q][col = g] for both column orders
+    double bop[3][2];
+#pragma unroll
+    for (int ax = 0; ax < 3; ++ax) {
+        const int m = g & 3, hi = g >> 2;
+        bop[ax][0] = hi ? p.A[ax][m][n + q] : p.A[ax][m][q];
+        bop[ax][1] = hi ? p.A[ax][m][q] : p.A[ax][m][n + q];
+    }
+
+    // global offsets of the nodes this warp copies (node = warp + WARPS * j); the periodic
+    // wrap is resolved once; each lane copies 16 B of the 512-B node block
+    int nodeoff[C::CPW];
+#pragma unroll
+    for (int j = 0; j < C::CPW; ++j) {
+        const int c = warp + WARPS * j;
+        const int ly = c / NX, lx = c - (c / NX) * NX;
+        int gx = cx0 + off + lx, gy = cy0 + off + ly;
+        gx %= M1; if (gx < 0) gx += M1;
+        gy %= M2; if (gy < 0) gy += M2;
+        nodeoff[j] = (gy * M1 + gx) * n3 + 2 * lane;
+    }
+    // node plane of the next copy, wrapped incrementally
+    int64_t gz_next = d.periodic_z ? wrap(zc0 + off, d.M3) : zc0 + off;
+    int issued = 0;
+    auto issue = [&]() {
+        if (issued < P) {
+            const double* base = src + gz_next * plane_elems;
+            double* Ub = U + (issued % STAGES) * C::U_D + 2 * lane;
+#pragma unroll
+            for (int j = 0; j < C::CPW; ++j)
+                if (NCOL % WARPS == 0 || warp + WARPS * j < NCOL)
+                    cp_async16(Ub + (warp + WARPS * j) * UNS, base + nodeoff[j]);
+            ++gz_next;
+            if (d.periodic_z && gz_next == d.M3) gz_next = 0;
+            ++issued;
+        }
+        cp_async_commit();
+    };
+#pragma unroll
+    for (int s = 0; s < STAGES - 1; ++s) issue();
+
+    // x3 chains: t = warp + WARPS * k -> (cell t >> 1, half t & 1).  obase: the lane's output
+    // offset in cell plane zc0 (m3 = 2 (q & 1) + i, line L), or -1 outside the grid.
+    int64_t obase[K3];
+#pragma unroll
+    for (int k = 0; k < K3; ++k) {
+        const int t = warp + WARPS * k;
+        const int cell = t >> 1, h = t & 1;
+        const int cx = cx0 + (cell % TX), cy = cy0 + cell / TX;
+        obase[k] = (cx < M1 && cy < M2)
+                       ? ((zc0 * M2 + cy) * (int64_t)M1 + cx) * n3 + (2 * (q & 1)) * 16 + 8 * h + g
+                       : -1;
+    }
+    double acc[K3][2];
+#pragma unroll
+    for (int k = 0; k < K3; ++k) acc[k][0] = acc[k][1] = 0.0;
+
+    for (int pl = 0; pl < P; ++pl) {
+        cp_async_wait<STAGES - 2>();
+        __syncthreads();
+        issue();  // the stage it fills was last read before the barrier above
+        const double* Ub = U + (pl % STAGES) * C::U_D;
+        double* V = C::VALIAS ? U + (pl % STAGES) * C::U_D : Vfix;
+
+        // ---- x1: (row ly, half h) chains walk the nodes of their row ------------------------
+        // Completed cells alternate between the lane halves; an even cell's values are
+        // held one node longer so both halves store together (full-warp STS).
+        {
+            const double* ua[K1];
+            double* wrow[K1];
+            bool live[K1];
+#pragma unroll
+            for (int j = 0; j < K1; ++j) {
+                const int t = warp + WARPS * j;
+                live[j] = C::T1 % WARPS == 0 || t < C::T1;
+                const int ly = live[j] ? t >> 1 : 0, h = t & 1;
+                const int L = 8 * h + g;  // line (j3, j2) = (L >> 2, L & 3)
+                ua[j] = Ub + ly * NX * UNS + L * 4 + q;
+                wrow[j] = W + ly * TX * WCS + (2 * h + (g >> 2)) * WRS + (g & 3) + (2 * (q & 1)) * 4;
+            }
+            double a[K1][NX];
+#pragma unroll
+            for (int j = 0; j < K1; ++j)
+#pragma unroll
+                for (int lx = 0; lx < NX; ++lx) a[j][lx] = live[j] ? ua[j][lx * UNS] : 0.0;
+            double r[K1][2], sv[K1][2];
+#pragma unroll
+            for (int j = 0; j < K1; ++j) r[j][0] = r[j][1] = sv[j][0] = sv[j][1] = 0.0;
+#pragma unroll
+            for (int lx = 0; lx < NX; ++lx) {
+                const bool done = par == ((lx + 1) & 1);  // cell lx-1 completed in these lanes
+#pragma unroll
+                for (int j = 0; j < K1; ++j) {
+                    dmma884(r[j][0], r[j][1], a[j][lx], bop[0][lx & 1]);
+                    if (lx & 1) {
+                        sv[j][0] = r[j][0];
+                        sv[j][1] = r[j][1];
+                    } else if (lx > 0 && live[j]) {
+                        double* w = wrow[j] + (lx - 1 - (par ^ 1)) * WCS;
+                        w[0] = par ? r[j][0] : sv[j][0];
+                        w[4] = par ? r[j][1] : sv[j][1];
+                    }
+                    r[j][0] = done ? 0.0 : r[j][0];
+                    r[j][1] = done ? 0.0 : r[j][1];
+                }
+            }
+        }
+        __syncthreads();
+
+        // ---- x2: (column ix, half h) chains walk the rows of their column -----------------
+        {
+            const double* wa[K2];
+            double* vcol[K2];
+            bool live[K2];
+#pragma unroll
+            for (int j = 0; j < K2; ++j) {
+                const int t = warp + WARPS * j;
+                live[j] = C::T2 % WARPS == 0 || t < C::T2;
+                const int ix = live[j] ? t >> 1 : 0, h = t & 1;
+                const int L = 8 * h + g;  // line (j3, m1) = (L >> 2, L & 3)
+                wa[j] = W + ix * WCS + (L >> 2) * WRS + (L & 3) * 4 + q;
+                vcol[j] = V + ix * VCS + (L & 3) * 4 + (L >> 2) + (2 * (q & 1)) * VRS;
+            }
+            double a[K2][NY];
+#pragma unroll
+            for (int j = 0; j < K2; ++j)
+#pragma unroll
+                for (int ly = 0; ly < NY; ++ly) a[j][ly] = live[j] ? wa[j][ly * TX * WCS] : 0.0;
+            double r[K2][2], sv[K2][2];
+#pragma unroll
+            for (int j = 0; j < K2; ++j) r[j][0] = r[j][1] = sv[j][0] = sv[j][1] = 0.0;
+#pragma unroll
+            for (int ly = 0; ly < NY; ++ly) {
+                const bool done = par == ((ly + 1) & 1);
+#pragma unroll
+                for (int j = 0; j < K2; ++j) {
+                    dmma884(r[j][0], r[j][1], a[j][ly], bop[1][ly & 1]);
+                    if (ly & 1) {
+                        if (ly == NY - 1) {  // lone last cell row: half-warp store
+                            if (done && live[j]) {
+                                double* v = vcol[j] + (ly - 1) * TX * VCS;
+                                v[0] = r[j][0];
+                                v[VRS] = r[j][1];
+                            }
+                        } else {
+                            sv[j][0] = r[j][0];
+                            sv[j][1] = r[j][1];
+                        }
+                    } else if (ly > 0 && live[j]) {
+                        double* v = vcol[j] + (ly - 1 - (par ^ 1)) * TX * VCS;
+                        v[0] = par ? r[j][0] : sv[j][0];
+                        v[VRS] = par ? r[j][1] : sv[j][1];
+                    }
+                    r[j][0] = done ? 0.0 : r[j][0];
+                    r[j][1] = done ? 0.0 : r[j][1];
+                }
+            }
+        }
+        __syncthreads();
+
+        // ---- x3: each warp advances its chains by one plane ---------------------------------
+        // Chain k runs with column phase (k & 1), so chains 2j and 2j+1 complete in opposite
+        // lane halves and share one full-warp store.
+        {
+            const int64_t plane_off = (int64_t)(pl - 1) * plane_elems;
+            double v0[K3], v1[K3];
+#pragma unroll
+            for (int k = 0; k < K3; ++k) {
+                const int t = warp + WARPS * k;
+                const int cell = t >> 1, h = t & 1;
+                const int L = 8 * h + g;  // line (m2, m1) = (L >> 2, L & 3)
+                const double a = V[cell * VCS + (L >> 2) * VRS + (L & 3) * 4 + q];
+                const int ph = (pl + k) & 1;
+                dmma884(acc[k][0], acc[k][1], a, ph ? bop[2][1] : bop[2][0]);
+                const bool done = par == ((pl + k + 1) & 1);
+                v0[k] = acc[k][0];
+                v1[k] = acc[k][1];
+                acc[k][0] = done ? 0.0 : acc[k][0];
+                acc[k][1] = done ? 0.0 : acc[k][1];
+            }
+            if (pl > 0) {
+#pragma unroll
+                for (int k = 0; k < K3; k += 2) {
+                    // lanes with par == ((pl + k + 1) & 1) hold chain k, the others chain k+1
+                    const bool mine = par == ((pl + k + 1) & 1);
+                    const bool pair = k + 1 < K3;
+                    if (!pair && !mine) continue;  // odd chain count: lone last chain
+                    const int k2 = pair ? k + 1 : k;
+                    const double o0 = mine ? v0[k] : v0[k2];
+                    const double o1 = mine ? v1[k] : v1[k2];
+                    const int64_t base = mine ? obase[k] : obase[k2];
+                    const bool bad = !isfinite(o0) || !isfinite(o1);
+                    if (base >= 0) {
+                        double* o = dst + base + plane_off;
+                        __stcs(o, o0);
+                        __stcs(o + 16, o1);
+                        if (bad) flag_bad(first_bad, (base + plane_off) / n3);
+                    }
+                }
+            }
+        }
+    }
+    cp_async_wait<0>();
+}
+
+template <class C>
+static int launch_dm3(const double* src, double* dst, const Dims& d, const SepOps<3>& ops, int off,
+                      cudaStream_t st, unsigned long long* first_bad,
+                      const unsigned long long* guard) {
+    const int64_t nz = d.z_end - d.z_begin;
+    auto kern = sep_fused_dmma3_kernel<C>;
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM);
+    if (e != cudaSuccess) return (int)e;
+    int per_sm = 0;
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, C::THREADS, C::SMEM);
+    if (e != cudaSuccess) return (int)e;
+    const int64_t gx = (d.M1 + C::TX - 1) / C::TX, gy = (d.M2 + C::TY - 1) / C::TY;
+    const int64_t want = (int64_t)num_sms() * (per_sm > 0 ? per_sm : 1) * 4;
+    int64_t zsplit = (want + gx * gy - 1) / (gx * gy);
+    int64_t zchunk = (nz + zsplit - 1) / zsplit;
+    if (zchunk < 8) zchunk = nz < 8 ? nz : 8;
+    const int64_t gz = (nz + zchunk - 1) / zchunk;
+    kern<<<dim3((unsigned)gx, (unsigned)gy, (unsigned)gz), C::THREADS, C::SMEM, st>>>(
+        src, dst, d, off, (int)zchunk, ops, first_bad, guard);
+    return (int)cudaGetLastError();
+}
+
+int sep_fused_dmma3_launch(const double* src, double* dst, const Dims& d, const double* A, int off,
+                           cudaStream_t st, unsigned long long* first_bad,
+                           const unsigned long long* guard) {
+    const int64_t nz = d.z_end - d.z_begin;
+    if (nz <= 0) return 0;
+    if (d.M1 * d.M2 * 64 >= (int64_t(1) << 31)) return (int)cudaErrorInvalidValue;
+    SepOps<3> ops;
+    for (int k = 0; k < 3; ++k)
+        for (int m = 0; m < 4; ++m)
+            for (int c = 0; c < 8; ++c) {
+                ops.A[k][m][c] = A[(k * 4 + m) * 8 + c];
+                ops.Sh[k][m][c] = 0.0;
+            }
+    // tile configuration (H3_DMMA_CFG selects alternatives for measurements)
+    static const int cfg = [] {
+        const char* e = getenv("H3_DMMA_CFG");
+        return e ? atoi(e) : 0;
+    }();
+    switch (cfg) {
+        case 1: return launch_dm3<Dm3Cfg<7, 16, 3, false>>(src, dst, d, ops, off, st, first_bad, guard);
+        case 2: return launch_dm3<Dm3Cfg<6, 16, 2, true, 2>>(src, dst, d, ops, off, st, first_bad, guard);
+        case 3: return launch_dm3<Dm3Cfg<6, 8, 2, true, 2>>(src, dst, d, ops, off, st, first_bad, guard);
+        case 4: return launch_dm3<Dm3Cfg<7, 16, 3, true>>(src, dst, d, ops, off, st, first_bad, guard);
+        case 5: return launch_dm3<Dm3Cfg<7, 8, 2, true>>(src, dst, d, ops, off, st, first_bad, guard);
+        default: return launch_dm3<Dm3Cfg<7, 16, 3, true>>(src, dst, d, ops, off, st, first_bad, guard);
+    }
+}
+
+}  // namespace h3

@@ -53,6 +53,9 @@ int literal_launch(int mode /*0 fused,1 recon,2 evolve*/, bool fast, const T* in
 int sep_fused_launch(const double* src, double* dst, const Dims& d, int order_n,
                      const double* A, int off, cudaStream_t st, unsigned long long* first_bad,
                      const unsigned long long* guard);
+int sep_fused_dmma3_launch(const double* src, double* dst, const Dims& d, const double* A, int off,
+                           cudaStream_t st, unsigned long long* first_bad,
+                           const unsigned long long* guard);
 int sep_evolve_launch(const double* coeff, double* dst, const Dims& d, int order_n,
                       const double* Sh, cudaStream_t st, unsigned long long* first_bad,
                       const unsigned long long* guard);

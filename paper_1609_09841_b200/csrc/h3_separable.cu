@@ -21,6 +21,9 @@
 //   4. the finished cell plane is stored with a fused finiteness check.
 // HBM traffic: each node block is read once and written once per half step
 // (32 B per DOF-update); the tile halo is re-read from L2.
+#include <cstdlib>
+#include <cstring>
+
 #include "h3_launch.h"
 
 namespace h3 {
@@ -274,7 +277,16 @@ int sep_fused_launch(const double* src, double* dst, const Dims& d, int order_n,
         case 0: return sep_fused_n<0>(src, dst, d, A, off, st, first_bad, guard);
         case 1: return sep_fused_n<1>(src, dst, d, A, off, st, first_bad, guard);
         case 2: return sep_fused_n<2>(src, dst, d, A, off, st, first_bad, guard);
-        case 3: return sep_fused_n<3>(src, dst, d, A, off, st, first_bad, guard);
+        case 3: {
+            // FP64 tensor-core kernel (h3_dmma.cu) unless H3_FUSED_IMPL=dfma asks for the
+            // DFMA kernel (kept for A/B measurements).
+            static const bool use_dfma = [] {
+                const char* e = getenv("H3_FUSED_IMPL");
+                return e && strcmp(e, "dfma") == 0;
+            }();
+            if (use_dfma) return sep_fused_n<3>(src, dst, d, A, off, st, first_bad, guard);
+            return sep_fused_dmma3_launch(src, dst, d, A, off, st, first_bad, guard);
+        }
         case 4: return sep_fused_n<4>(src, dst, d, A, off, st, first_bad, guard);
         case 5: return sep_fused_n<5>(src, dst, d, A, off, st, first_bad, guard);
     }

@@ -5,20 +5,21 @@ phases of 128 / w lanes, and a phase costs as many wavefronts as the largest num
 distinct 16-B (w = 16) or 8-B (w = 8) words that fall into the same bank group.
 
 Layouts (doubles):
-  U node  [j3][j2][j1]   j3 stride UJ,  node stride UNS   (staged input plane, cp.async 16 B)
-  W node  [j3][m1][j2]   j3 stride WJ,  node stride WNS   (pass-x1 output)
+  V node  [m3][j2][j1]   m3 stride UJ,  node stride UNS   (x3-contracted node plane)
+  W node  [m3][m1][j2]   m3 stride WJ,  node stride WNS   (pass-x1 output)
 Access patterns simulated (exactly as the kernel maps threads):
-  x1 load   : thread t owns line L = t + r*T -> (ly, ix, j3, j2); reads n doubles of node ix and ix+1
+  x3 store  : task t = tid + r*T -> (column t / n^2, line t % n^2); writes V[col][m3][line] (8 B)
+  x1 load   : task L -> (ly, ix, m3, j2); reads n doubles of node ix and ix+1
               in 16-B pieces (or 8-B when n is odd)
-  x1 store  : same lines, writes W[ly][ix][j3][m1][j2] (8 B) for each m1
-  x2 load   : thread t -> (m1, ix, iy); reads W[iy + a][ix][j3][m1][0..n) in 16-B / 8-B pieces
-  fill      : cp.async chunk e = t + r*T -> node e / CPN, piece e % CPN (16 B)
+  x1 store  : same tasks, writes W[ly][ix][m3][m1][j2] (8 B) for each m1
+  x2 load   : task t -> (m1, ix, m3, iy); reads W[iy + a][ix][m3][m1][0..n) in 16-B / 8-B pieces
 Prints the best (UJ, UNS, WJ, WNS) per order N for the tile sizes in h3_separable.cu.
 """
 
 import itertools
 
-TILES = {0: (32, 8), 1: (16, 8), 2: (8, 8), 3: (8, 8), 4: (8, 4), 5: (8, 4)}
+# (TX, TY, THREADS) per order N, as in SepTile<N> (h3_separable.cu)
+TILES = {0: (32, 8, 256), 1: (16, 16, 1024), 2: (8, 8, 768), 3: (8, 8, 1024), 4: (8, 4, 576), 5: (8, 4, 384)}
 
 
 def phase_cost(addrs_bytes, width):
@@ -44,9 +45,8 @@ def ideal(addrs_bytes, width):
 
 def evaluate(N, UJ, UNS, WJ, WNS):
     n = N + 1
-    TX, TY = TILES[N]
+    TX, TY, T = TILES[N]
     NX, NY = TX + 1, TY + 1
-    T = TX * TY * n
     L1 = NY * TX * n * n
     vec = 2 if (n * n * n) % 2 == 0 and n % 2 == 0 else 1
     w = 8 * vec
@@ -73,53 +73,49 @@ def evaluate(N, UJ, UNS, WJ, WNS):
             cost += phase_cost(ad, 8)
             ideal_cost += ideal(ad, 8)
     # x2 loads
-    for base in range(0, T, 32):
+    L2 = TY * TX * n * n
+    for base in range(0, ((L2 + T - 1) // T) * T, 32):
         dec = []
         for t in range(base, base + 32):
-            if t >= T:
+            if t >= L2:
                 dec.append(None)
                 continue
-            dec.append((t % n, (t // n) % TX, t // (n * TX)))
+            dec.append((t % n, (t // n) % TX, (t // (n * TX)) % n, t // (n * TX * n)))
         for a2 in (0, 1):
-            for j3 in range(n):
-                for h in range(n // vec):
-                    ad = [None if d is None else 8 * (((d[2] + a2) * TX + d[1]) * WNS + j3 * WJ + d[0] * n + h * vec) for d in dec]
-                    cost += phase_cost(ad, w)
-                    ideal_cost += ideal(ad, w)
-    # cp.async fill (16 B pieces when possible)
-    fvec = 2 if (n ** 3) % 2 == 0 and UJ % 2 == 0 and UNS % 2 == 0 else 1
-    cpn = n ** 3 // fvec
-    per_row = n * n // fvec if (n * n) % fvec == 0 else None
-    ncopy = NY * NX * cpn
-    for base in range(0, ((ncopy + T - 1) // T) * T, 32):
-        ad = []
-        for e in range(base, base + 32):
-            if e >= ncopy:
-                ad.append(None)
-                continue
-            node, pc = divmod(e, cpn)
-            dbl = pc * fvec
-            j3, r = divmod(dbl, n * n)
-            ad.append(8 * (node * UNS + j3 * UJ + r))
-        cost += phase_cost(ad, 8 * fvec)
-        ideal_cost += ideal(ad, 8 * fvec)
+            for h in range(n // vec):
+                ad = [None if d is None else 8 * (((d[3] + a2) * TX + d[1]) * WNS + d[2] * WJ + d[0] * n + h * vec) for d in dec]
+                cost += phase_cost(ad, w)
+                ideal_cost += ideal(ad, w)
+    # x3 stores into V
+    L3 = NY * NX * n * n
+    for base in range(0, ((L3 + T - 1) // T) * T, 32):
+        for m3 in range(n):
+            ad = []
+            for t in range(base, base + 32):
+                if t >= L3:
+                    ad.append(None)
+                    continue
+                col, line = divmod(t, n * n)
+                ad.append(8 * (col * UNS + m3 * UJ + line))
+            cost += phase_cost(ad, 8)
+            ideal_cost += ideal(ad, 8)
     return cost, ideal_cost
 
 
 def search(N):
     n = N + 1
     best = None
-    for pu, pn, pw, pv in itertools.product(range(0, 6), range(0, 6), range(0, 6), range(0, 6)):
+    for pu, pn, pw, pv in itertools.product(range(0, 5), range(0, 5), range(0, 5), range(0, 5)):
         UJ = n * n + pu
         UNS = n * UJ + pn
         WJ = n * n + pw
         WNS = n * WJ + pv
-        if (n ** 3) % 2 == 0 and (UJ % 2 or UNS % 2):
-            continue  # keep 16-B alignment for cp.async 16
+        if n % 2 == 0 and (UJ % 2 or UNS % 2):
+            continue  # 16-B vector loads of V lines
         if n % 2 == 0 and (WJ % 2 or WNS % 2):
             continue  # 16-B vector loads of W rows
         c, ic = evaluate(N, UJ, UNS, WJ, WNS)
-        smem = 8 * (2 * (TILES[N][0] + 1) * (TILES[N][1] + 1) * UNS + (TILES[N][1] + 1) * TILES[N][0] * WNS)
+        smem = 8 * ((TILES[N][0] + 1) * (TILES[N][1] + 1) * UNS + (TILES[N][1] + 1) * TILES[N][0] * WNS)
         key = (c, smem)
         if best is None or key < best[0]:
             best = (key, (UJ, UNS, WJ, WNS), ic)
