@@ -59,6 +59,19 @@ def parse():
 
 # ----------------------------------------------------------------------------- helpers
 
+def measured_traffic(order_n, cells, mode, variant):
+    """DRAM bytes per launch of the dominant kernel from the committed ncu capture
+    (profiles/*_summary.json), when that capture is of this exact workload."""
+    if (order_n, cells, mode, variant) != (3, 512, "fused", "separable"):
+        return None, None
+    p = ROOT / "profiles" / "r01_sep_fused_dmma3_512_summary.json"
+    if not p.exists():
+        return None, None
+    d = json.loads(p.read_text())
+    gb = float(d["dram__bytes_read.sum"]["value"]) + float(d["dram__bytes_write.sum"]["value"])
+    return gb * 1e9, str(p.relative_to(ROOT))
+
+
 def peaks():
     p = ROOT / "MEASURED_PEAKS.json"
     if p.exists():
@@ -273,6 +286,7 @@ def main():
     achieved = alg_bytes / (launch_ms / 1e3) / 1e9 if launch_ms else None
 
     flag_bad = int(flags[0].item()) if world == 1 else -1
+    traffic, traffic_src = measured_traffic(order_n, m, args.mode, args.variant)
     result = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
@@ -285,8 +299,11 @@ def main():
                    "mode": args.mode, "variant": args.variant, "parallelism": f"slab-x3 x{world}",
                    "l2": f"inputs larger than L2 ({dofs_per_step // world * 8 / 1e9:.1f} GB per field vs 126 MB L2)"},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak_gbs, "unit": "GB/s",
-                     "frac": (achieved / peak_gbs) if achieved else None, "traffic": None,
-                     "kernel": "sep_fused_kernel<3,8,8,4>" if args.mode == "fused" else "recon+evolve",
+                     "frac": (achieved / peak_gbs) if achieved else None, "traffic": traffic,
+                     "traffic_unit": "DRAM bytes per launch (ncu dram__bytes_read+write)",
+                     "traffic_source": traffic_src,
+                     "kernel": ("sep_fused_dmma3_kernel (DMMA m8n8k4, 8x7 tile, 16 warps)" if order_n == 3
+                                else f"sep_fused_kernel<{order_n}>") if args.mode == "fused" else "recon+evolve",
                      "algorithmic_bytes_per_launch": alg_bytes, "mean_launch_ms": launch_ms,
                      "peak_source": peak_src},
         "gpu_launches": launches_per_step * args.steps,
@@ -295,14 +312,18 @@ def main():
     result["clocks"] = clocks.summary()
 
     # ---- e2e through the package API with host-resident state (1 GPU) ---------------------
+    print(f"[bench] value {value:.4e} DOF-updates/s, kernel {launch_ms} ms", file=sys.stderr, flush=True)
     if world == 1 and not args.no_e2e:
         result["e2e"] = e2e_host(hb, torch, state, scratch, cfg, ops, dt, args.e2e_steps, dofs_per_step)
+        print(f"[bench] e2e {result['e2e']}", file=sys.stderr, flush=True)
     # ---- CPU baseline (rank 0, N = 1) ----------------------------------------------------------
     if world == 1 and not args.no_cpu:
         rate, info = cpu_oracle_rate(order_n, cpu_sample_cells(order_n), args.cpu_seconds)
         result["cpu_baseline"] = {"value": rate, "unit": UNIT, "cores": info["cores"], "kind": "port",
                                   "sample": info["sample"]}
     if world == 1 and args.extras:
+        del state, scratch
+        torch.cuda.empty_cache()
         result["extras"] = extras(hb, torch, order_n)
     if rank == 0:
         print(json.dumps(result), flush=True)
