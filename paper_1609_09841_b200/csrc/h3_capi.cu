@@ -2,6 +2,7 @@
 // host-side separable operator math.  Everything here is plain C++; the
 // kernels live in h3_literal.cu, h3_separable.cu and h3_problems.cu.
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 
 #include "../../include/h3b200.h"
@@ -111,6 +112,16 @@ static int recon_impl(const T* src, T* coeff, int64_t M1, int64_t M2, int64_t M3
         default: return H3_ERR_VARIANT;
     }
     Dims d{M1, M2, M3, z_begin, z_end, periodic_z ? 1 : 0};
+    if (fast && sizeof(T) == 8 && order_n == 3) {
+        // node-factorised FP64 tensor-core reconstruction (H3_RECON_IMPL=fma: per-cell sweeps)
+        static const bool use_fma = [] {
+            const char* e = getenv("H3_RECON_IMPL");
+            return e && strcmp(e, "fma") == 0;
+        }();
+        if (!use_fma)
+            return h3::recon_dmma3_launch((const double*)src, (double*)coeff, d, (const double*)h_mat, off,
+                                          reinterpret_cast<cudaStream_t>(stream), d_guard);
+    }
     return h3::literal_launch<T>(1, fast, src, coeff, d, order_n, h_mat, nullptr, nullptr, nullptr,
                                  nullptr, 1, off, reinterpret_cast<cudaStream_t>(stream), nullptr,
                                  d_guard);

@@ -298,96 +298,108 @@ int sep_fused_launch(const double* src, double* dst, const Dims& d, int order_n,
 // out[m3][m2][m1] = sum S3[m3][i3] S2[m2][i2] S1[m1][i1] coeff[i3][i2][i1], applied axis by
 // axis (s^3 n + s^2 n^2 + s n^3 FMAs per cell).  S_k are the exact shift rows of
 // exp(delta d/dx_k); equal to the reference's q-stage Horner for q >= 3(2N+1).
-// CTA = CPB consecutive cells (contiguous in the chunked coefficient field).
+//
+// Streaming design: one CTA per group of CPB consecutive cells; one thread per
+// (cell, x1-line) reads its s contiguous coefficients straight from HBM into registers
+// (16-B loads; a warp reads 2 KB contiguous), contracts them to n values (pass x1), and the
+// small x2/x3 passes run through shared memory.  Many small CTAs per SM keep the loads
+// in flight.
 template <int N>
-constexpr int ev_cpb() { return N <= 1 ? 16 : (N <= 3 ? 4 : 2); }
+constexpr int ev_cpb() { return (2 * N + 2) * (2 * N + 2) >= 256 ? 1 : 256 / ((2 * N + 2) * (2 * N + 2)); }
 
 template <int N, int CPB>
 __global__ void __launch_bounds__(CPB*(2 * N + 2) * (2 * N + 2))
 sep_evolve_kernel(const double* __restrict__ coeff, double* __restrict__ dst, Dims d,
                   const __grid_constant__ SepOps<N> p, unsigned long long* first_bad,
                   const unsigned long long* guard) {
-    constexpr int n = N + 1, S = 2 * n, S2 = S * S, S3 = S2 * S, n3 = n * n * n;
+    constexpr int n = N + 1, S = 2 * n, S2 = S * S, S3 = S2 * S, n2 = n * n, n3 = n2 * n;
     constexpr int THREADS = CPB * S2;
+    constexpr int T1S = S2 * n + 1;  // per-cell stride of the pass-x1 output (odd: spreads banks)
+    constexpr int T2S = S * n2 + 1;
     if (guarded_out(guard, first_bad)) return;
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    double* C = reinterpret_cast<double*>(smem_raw);  // CPB * S3
-    double* T1 = C + CPB * S3;                          // CPB * S*S*n   [c][i3][i2][m1]
-    double* T2 = T1 + CPB * S2 * n;                     // CPB * S*n*n   [c][i3][m2][m1]
+    __shared__ double T1[CPB * T1S];  // [c][i3][i2][m1]
+    __shared__ double T2[CPB * T2S];  // [c][i3][m2][m1]
 
     const int64_t nxy = d.M1 * d.M2;
     const int64_t total = (d.z_end - d.z_begin) * nxy;
-    const int64_t cell0 = (int64_t)blockIdx.x * CPB;
-    const int ncell = (int)min((int64_t)CPB, total - cell0);
+    const int64_t groups = (total + CPB - 1) / CPB;
     const int tid = threadIdx.x;
-    {
-        const double* g = coeff + cell0 * S3;
-        const int count = ncell * S3 / 2;  // S3 is even
-        for (int e = tid; e < count; e += THREADS) cp_async16(C + 2 * e, g + 2 * e);
-        cp_async_commit();
-        cp_async_wait<0>();
-    }
-    __syncthreads();
-    // pass x1: lines (c, i3, i2) -> n outputs m1
-    {
-        const int c = tid / S2, line = tid % S2;
-        const double* in = C + c * S3 + line * S;
-        double u[S];
+    const int c = tid / S2, line = tid - (tid / S2) * S2;  // x1 task: (cell, line (i3, i2))
+
+    double u[S];
+    auto load = [&](int64_t grp) {
+        const int64_t cell = grp * CPB + c;
+        if (grp < groups && cell < total) {
+            const double2* g2 = reinterpret_cast<const double2*>(coeff + cell * S3 + line * S);
 #pragma unroll
-        for (int k = 0; k < S; ++k) u[k] = in[k];
+            for (int k = 0; k < S / 2; ++k) {
+                const double2 v = __ldcs(g2 + k);
+                u[2 * k] = v.x;
+                u[2 * k + 1] = v.y;
+            }
+        } else {
+#pragma unroll
+            for (int k = 0; k < S; ++k) u[k] = 0.0;
+        }
+    };
+    const int64_t grp = blockIdx.x;
+    load(grp);
+    {
+        // pass x1 (registers): T1[c][i3][i2][m1] = sum_i1 S1[m1][i1] u[i1]
 #pragma unroll
         for (int m = 0; m < n; ++m) {
             double acc = p.Sh[0][m][0] * u[0];
 #pragma unroll
             for (int k = 1; k < S; ++k) acc = fma(p.Sh[0][m][k], u[k], acc);
-            T1[(c * S2 + line) * n + m] = acc;
+            T1[c * T1S + line * n + m] = acc;
         }
-    }
-    __syncthreads();
-    // pass x2: lines (c, i3, m1) -> n outputs m2
-    for (int l = tid; l < CPB * S * n; l += THREADS) {
-        const int c = l / (S * n), r = l % (S * n), i3 = r / n, mm1 = r % n;
-        double u[S];
+        __syncthreads();
+        // pass x2: (c, i3, m1) -> n outputs m2
+        for (int l = tid; l < CPB * S * n; l += THREADS) {
+            const int cc = l / (S * n), r = l - cc * (S * n), i3 = r / n, mm1 = r - (r / n) * n;
+            double a[S];
 #pragma unroll
-        for (int k = 0; k < S; ++k) u[k] = T1[((c * S + i3) * S + k) * n + mm1];
+            for (int k = 0; k < S; ++k) a[k] = T1[cc * T1S + (i3 * S + k) * n + mm1];
 #pragma unroll
-        for (int m = 0; m < n; ++m) {
-            double acc = p.Sh[1][m][0] * u[0];
+            for (int m = 0; m < n; ++m) {
+                double acc = p.Sh[1][m][0] * a[0];
 #pragma unroll
-            for (int k = 1; k < S; ++k) acc = fma(p.Sh[1][m][k], u[k], acc);
-            T2[((c * S + i3) * n + m) * n + mm1] = acc;
+                for (int k = 1; k < S; ++k) acc = fma(p.Sh[1][m][k], a[k], acc);
+                T2[cc * T2S + (i3 * n + m) * n + mm1] = acc;
+            }
         }
-    }
-    __syncthreads();
-    // pass x3: lines (c, m2, m1) -> n outputs m3, stored to the destination node
-    for (int l = tid; l < CPB * n * n; l += THREADS) {
-        const int c = l / (n * n), r = l % (n * n);
-        if (c >= ncell) continue;
-        double u[S];
+        __syncthreads();
+        // pass x3: (c, m2, m1) -> n outputs m3, stored to the destination node
+        for (int l = tid; l < CPB * n2; l += THREADS) {
+            const int cc = l / n2, r = l - cc * n2;
+            const int64_t cell = grp * CPB + cc;
+            if (cell >= total) continue;
+            double a[S];
 #pragma unroll
-        for (int k = 0; k < S; ++k) u[k] = T2[(c * S + k) * n * n + r];
-        const int64_t cell = cell0 + c;
-        const int64_t crel3 = cell / nxy, rem = cell - crel3 * nxy;
-        const int64_t node = ((d.z_begin + crel3) * d.M2 + rem / d.M1) * d.M1 + rem % d.M1;
-        double* o = dst + node * n3 + r;
-        bool bad = false;
+            for (int k = 0; k < S; ++k) a[k] = T2[cc * T2S + k * n2 + r];
+            const int64_t crel3 = cell / nxy, rem = cell - crel3 * nxy;
+            const int64_t node = ((d.z_begin + crel3) * d.M2 + rem / d.M1) * d.M1 + rem % d.M1;
+            double* o = dst + node * n3 + r;
+            bool bad = false;
 #pragma unroll
-        for (int m = 0; m < n; ++m) {
-            double acc = p.Sh[2][m][0] * u[0];
+            for (int m = 0; m < n; ++m) {
+                double acc = p.Sh[2][m][0] * a[0];
 #pragma unroll
-            for (int k = 1; k < S; ++k) acc = fma(p.Sh[2][m][k], u[k], acc);
-            o[m * n * n] = acc;
-            bad |= !isfinite(acc);
+                for (int k = 1; k < S; ++k) acc = fma(p.Sh[2][m][k], a[k], acc);
+                __stcs(o + m * n2, acc);
+                bad |= !isfinite(acc);
+            }
+            if (bad) flag_bad(first_bad, node);
         }
-        if (bad) flag_bad(first_bad, node);
+        __syncthreads();
     }
 }
 
-template <int N>
-static int sep_evolve_n(const double* coeff, double* dst, const Dims& d, const double* Sh,
+template <int N, int CPB>
+static int sep_evolve_nc(const double* coeff, double* dst, const Dims& d, const double* Sh,
                         cudaStream_t st, unsigned long long* first_bad,
                         const unsigned long long* guard) {
-    constexpr int n = N + 1, S = 2 * n, S2 = S * S, S3 = S2 * S, CPB = ev_cpb<N>();
+    constexpr int n = N + 1, S = 2 * n, S2 = S * S;
     const int64_t total = (d.z_end - d.z_begin) * d.M1 * d.M2;
     if (total <= 0) return 0;
     SepOps<N> ops;
@@ -397,13 +409,26 @@ static int sep_evolve_n(const double* coeff, double* dst, const Dims& d, const d
                 ops.Sh[k][m][c] = Sh[(k * n + m) * S + c];
                 ops.A[k][m][c] = 0.0;
             }
-    const size_t smem = (size_t)CPB * (S3 + S2 * n + S * n * n) * sizeof(double);
     auto kern = sep_evolve_kernel<N, CPB>;
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return (int)e;
-    const int64_t blocks = (total + CPB - 1) / CPB;
-    kern<<<(unsigned)blocks, CPB * S2, smem, st>>>(coeff, dst, d, ops, first_bad, guard);
+    const int64_t groups = (total + CPB - 1) / CPB;
+    kern<<<(unsigned)groups, CPB * S2, 0, st>>>(coeff, dst, d, ops, first_bad, guard);
     return (int)cudaGetLastError();
+}
+
+template <int N>
+static int sep_evolve_n(const double* coeff, double* dst, const Dims& d, const double* Sh,
+                        cudaStream_t st, unsigned long long* first_bad,
+                        const unsigned long long* guard) {
+    if constexpr (N == 3) {
+        static const int cpb = [] {
+            const char* e = getenv("H3_EVOLVE_CPB");
+            return e ? atoi(e) : 8;
+        }();
+        if (cpb == 4) return sep_evolve_nc<3, 4>(coeff, dst, d, Sh, st, first_bad, guard);
+        if (cpb == 2) return sep_evolve_nc<3, 2>(coeff, dst, d, Sh, st, first_bad, guard);
+        return sep_evolve_nc<3, 8>(coeff, dst, d, Sh, st, first_bad, guard);
+    }
+    return sep_evolve_nc<N, ev_cpb<N>()>(coeff, dst, d, Sh, st, first_bad, guard);
 }
 
 int sep_evolve_launch(const double* coeff, double* dst, const Dims& d, int order_n,
