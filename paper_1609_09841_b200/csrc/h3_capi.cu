@@ -112,15 +112,22 @@ static int recon_impl(const T* src, T* coeff, int64_t M1, int64_t M2, int64_t M3
         default: return H3_ERR_VARIANT;
     }
     Dims d{M1, M2, M3, z_begin, z_end, periodic_z ? 1 : 0};
-    if (fast && sizeof(T) == 8 && order_n == 3) {
-        // node-factorised FP64 tensor-core reconstruction (H3_RECON_IMPL=fma: per-cell sweeps)
-        static const bool use_fma = [] {
+    if (fast && sizeof(T) == 8) {
+        // node-factorised reconstruction: FP64 tensor cores at N = 3, DFMA otherwise
+        // (H3_RECON_IMPL=sep: DFMA kernel at N = 3 too; =fma: per-cell sweeps, for A/B runs)
+        static const int impl = [] {
             const char* e = getenv("H3_RECON_IMPL");
-            return e && strcmp(e, "fma") == 0;
+            if (e && strcmp(e, "fma") == 0) return 2;
+            if (e && strcmp(e, "sep") == 0) return 1;
+            return 0;
         }();
-        if (!use_fma)
-            return h3::recon_dmma3_launch((const double*)src, (double*)coeff, d, (const double*)h_mat, off,
-                                          reinterpret_cast<cudaStream_t>(stream), d_guard);
+        cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+        if (impl == 0 && order_n == 3)
+            return h3::recon_dmma3_launch((const double*)src, (double*)coeff, d, (const double*)h_mat, off, st,
+                                          d_guard);
+        if (impl != 2)
+            return h3::recon_sep_launch((const double*)src, (double*)coeff, d, order_n, (const double*)h_mat, off,
+                                        st, d_guard);
     }
     return h3::literal_launch<T>(1, fast, src, coeff, d, order_n, h_mat, nullptr, nullptr, nullptr,
                                  nullptr, 1, off, reinterpret_cast<cudaStream_t>(stream), nullptr,

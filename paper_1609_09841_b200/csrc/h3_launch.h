@@ -58,6 +58,8 @@ int sep_fused_dmma3_launch(const double* src, double* dst, const Dims& d, const 
                            const unsigned long long* guard);
 int recon_dmma3_launch(const double* src, double* coeff, const Dims& d, const double* h_mat, int off,
                        cudaStream_t st, const unsigned long long* guard);
+int recon_sep_launch(const double* src, double* coeff, const Dims& d, int order_n, const double* h_mat,
+                     int off, cudaStream_t st, const unsigned long long* guard);
 int sep_evolve_launch(const double* coeff, double* dst, const Dims& d, int order_n,
                       const double* Sh, cudaStream_t st, unsigned long long* first_bad,
                       const unsigned long long* guard);

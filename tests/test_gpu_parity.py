@@ -331,31 +331,62 @@ def test_slab_solver_single_rank_matches_periodic(order_n, cells):
     assert torch.equal(solver.state, state.tensor)
 
 
+RECON_TOL = {0: 1e-13, 1: 1e-13, 2: 1e-13, 3: 1e-13, 4: 1e-12, 5: 1e-12}
+
+
+@pytest.mark.parametrize("order_n", [0, 1, 2, 3, 4, 5])
 @pytest.mark.parametrize("cells,off", [((16, 12, 10), 0), ((9, 7, 5), -1), ((8, 8, 8), 0), ((1, 3, 2), -1)])
-def test_fast_recon_coefficients_match_reference(cells, off):
-    """The fast reconstruction (node-factorised DMMA at N=3) equals the reference's
-    coefficient field (literal recon, bit-identical to gridkernels.recon_pass) to FP64 noise."""
-    n = 3
+def test_fast_recon_coefficients_match_reference(cells, off, order_n):
+    """The fast reconstruction (node-factorised: DMMA at N=3, constant-operand DFMA otherwise)
+    equals the reference's coefficient field (literal recon, bit-identical to
+    gridkernels.recon_pass) to FP64 noise, including ragged tiles and 1-cell axes."""
+    n = order_n
     m1, m2, m3 = cells
-    src = np.random.default_rng(9).uniform(-1, 1, (m3, m2, m1, 4, 4, 4))
+    nn, s = n + 1, 2 * n + 2
+    src = np.random.default_rng(9).uniform(-1, 1, (m3, m2, m1, nn, nn, nn))
     d_src = torch.from_numpy(src).cuda()
     h_mat = np.ascontiguousarray(rm.interp_matrix(n))
     outs = []
     for variant in ("literal", "separable"):
-        coeff = torch.empty((m3, m2, m1, 8, 8, 8), dtype=torch.float64, device="cuda")
+        coeff = torch.empty((m3, m2, m1, s, s, s), dtype=torch.float64, device="cuda")
         rc = _native.lib().h3_recon_pass(ctypes.c_void_p(d_src.data_ptr()), ctypes.c_void_p(coeff.data_ptr()),
                                          m1, m2, m3, n, h_mat.ctypes.data_as(ctypes.c_void_p), off,
                                          0, m3, 1, _native.VARIANTS[variant], None, None)
         assert rc == 0
         torch.cuda.synchronize()
         outs.append(coeff.cpu().numpy())
-    assert rm.rel_err(outs[1], outs[0]) <= 1e-13
+    assert rm.rel_err(outs[1], outs[0]) <= RECON_TOL[n]
     # and the chunked (slab range) reconstruction writes only its cells, chunk-relative
     z0, z1 = m3 // 2, m3
-    coeff = torch.full((z1 - z0, m2, m1, 8, 8, 8), np.nan, dtype=torch.float64, device="cuda")
+    coeff = torch.full((z1 - z0, m2, m1, s, s, s), np.nan, dtype=torch.float64, device="cuda")
     rc = _native.lib().h3_recon_pass(ctypes.c_void_p(d_src.data_ptr()), ctypes.c_void_p(coeff.data_ptr()),
                                      m1, m2, m3, n, h_mat.ctypes.data_as(ctypes.c_void_p), off,
                                      z0, z1, 1, _native.VARIANTS["separable"], None, None)
     assert rc == 0
     torch.cuda.synchronize()
-    assert rm.rel_err(coeff.cpu().numpy(), outs[0][z0:z1]) <= 1e-13
+    assert rm.rel_err(coeff.cpu().numpy(), outs[0][z0:z1]) <= RECON_TOL[n]
+
+
+def test_constant_operator_ring_many_operator_sets():
+    """More distinct operator sets than constant slots, interleaved on two streams: every
+    launch must see its own operators (slot reuse waits for the previous users)."""
+    n, cells = 1, (6, 5, 4)
+    nn = n + 1
+    src = torch.from_numpy(np.random.default_rng(3).uniform(-1, 1, (4, 5, 6, nn, nn, nn))).cuda()
+    base = np.ascontiguousarray(rm.interp_matrix(n))
+    streams = [torch.cuda.Stream(), torch.cuda.Stream()]
+    outs, refs = [], []
+    for k in range(9):
+        h = np.ascontiguousarray(base * (1.0 + 0.125 * k))
+        for variant, bucket in (("separable", outs), ("literal", refs)):
+            coeff = torch.empty((4, 5, 6, 4, 4, 4), dtype=torch.float64, device="cuda")
+            st = streams[k % 2]
+            st.wait_stream(torch.cuda.current_stream())
+            rc = _native.lib().h3_recon_pass(ctypes.c_void_p(src.data_ptr()), ctypes.c_void_p(coeff.data_ptr()),
+                                             *cells, n, h.ctypes.data_as(ctypes.c_void_p), 0, 0, 4, 1,
+                                             _native.VARIANTS[variant], ctypes.c_void_p(st.cuda_stream), None)
+            assert rc == 0
+            bucket.append(coeff)
+    torch.cuda.synchronize()
+    for a, b in zip(outs, refs):
+        assert rm.rel_err(a.cpu().numpy(), b.cpu().numpy()) <= 1e-13
