@@ -1,0 +1,293 @@
+// FP64 tensor-core (DMMA m8n8k4) fused half step for orders with 2n % 4 == 0 (N = 5: n = 6).
+//
+// Same exact separable local evolution as the other fused kernels,
+//     out(c) = sum_a (A3^a3 (x) A2^a2 (x) A1^a1) u(c + off + a),
+// applied as three 1-D passes, but in "cell-pair" form: a line of a pass gathers its cell's two
+// vertex blocks (2n = 12 inputs, both nodes along the pass axis) and contracts them with
+// [A^0 | A^1] (n x 2n) into the cell's n outputs.  As a GEMM: D[line][m] = sum_k X[line][k] B[k][m]
+// with K = 2n = 12 = three m8n8k4 k-steps and N = n = 6 of the 8 columns (75 % of the MMA is
+// useful).  The alternative, node-factorised form (K = n = 6, N = 2n = 12) would fill only
+// 56 %; DFMA with the operators in registers spills (255 registers, 36 % of HBM measured).
+// Nothing is carried between MMAs, so there is no per-lane bookkeeping: every pass is
+// "3 x LDS, 3 x DMMA, 2 x store" per 8 lines.
+//
+// CTA = TX x TY cells in (x1, x2), 16 warps, marching along x3 over a chunk of cell planes.
+// Per node plane p (staged by TMA bulk row copies, 3-stage mbarrier ring):
+//   x1: line (node row ly, cell cx, j3 j2)   U(p) -> W[ly][cx][m1][j3 j2]
+//   x2: line (cell, j3, m1)                  W    -> V[p & 1][cell][j3][m2 m1]
+//   x3: line (cell, m2 m1), planes p-1 and p V[(p-1) & 1], V[p & 1] -> dst (cell plane p-1)
+// V is double-buffered so x3 pairs the planes without a register accumulator.
+#include <cstdlib>
+
+#include "h3_launch.h"
+
+namespace h3 {
+
+namespace cp5 {
+
+__device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b) {
+    asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+        : "+d"(d0), "+d"(d1)
+        : "d"(a), "d"(b));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_fence_init() { asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory"); }
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, unsigned bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
+    asm volatile(
+        "{\n.reg .pred p;\nWAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        "@!p bra WAIT_%=;\n}\n" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(double* sdst, const double* gsrc, unsigned bytes, uint64_t* bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+                     smem_u32(sdst)),
+                 "l"(gsrc), "r"(bytes), "r"(smem_u32(bar))
+                 : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async_smem() { asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory"); }
+
+template <int N_, int TX_, int TY_>
+struct Cfg {
+    static constexpr int N = N_, n = N + 1, n2 = n * n, n3 = n2 * n, K2 = 2 * n;
+    static constexpr int KS = K2 / 4;  // m8n8k4 k-steps per line
+    static_assert(K2 % 4 == 0, "cell-pair form needs 2n divisible by 4");
+    static_assert(n <= 8, "n outputs must fit the 8 MMA columns");
+    static constexpr int TX = TX_, TY = TY_, NX = TX + 1, NY = TY + 1, NNODE = NX * NY;
+    static constexpr int WARPS = 16, THREADS = 32 * WARPS, STAGES = 3;
+    static constexpr int UNS = n3;                   // U: dense node blocks [j3][j2][j1]
+    static constexpr int WM = n2 + 1, WCS = n * WM;  // W: [node row][cell][m1][j3 j2], odd m1 stride
+    static constexpr int VJ = n2 + 1, VCS = n * VJ;  // V: [cell][j3][m2 m1]
+    static constexpr int G1 = (NY * TX * n2 + 7) / 8;  // x1 line groups of 8
+    static constexpr int G2 = (TY * TX * n2 + 7) / 8;  // x2 line groups
+    static constexpr int G3 = (TY * TX * n2 + 7) / 8;  // x3 line groups
+    static constexpr size_t U_D = (size_t)NNODE * UNS;
+    static constexpr size_t W_D = (size_t)NY * TX * WCS;
+    static constexpr size_t V_D = (size_t)TY * TX * VCS;
+    static constexpr size_t SMEM_DATA = (STAGES * U_D + W_D + 2 * V_D) * sizeof(double);
+    static constexpr size_t SMEM = SMEM_DATA + STAGES * sizeof(uint64_t);
+    static_assert(NY <= WARPS, "one loader warp per tile row");
+};
+
+}  // namespace cp5
+
+template <class C>
+__global__ void __launch_bounds__(C::THREADS, 1)
+sep_fused_dmma_cp_kernel(const double* __restrict__ src, double* __restrict__ dst, Dims d, int off, int zchunk,
+                         const __grid_constant__ SepOps<C::N> p, unsigned long long* first_bad,
+                         const unsigned long long* guard) {
+    using namespace cp5;
+    constexpr int n = C::n, n2 = C::n2, n3 = C::n3, KS = C::KS, TX = C::TX, TY = C::TY, NX = C::NX, NY = C::NY;
+    constexpr int WARPS = C::WARPS, STAGES = C::STAGES, UNS = C::UNS, WM = C::WM, WCS = C::WCS;
+    constexpr int VJ = C::VJ, VCS = C::VCS;
+    constexpr int L1 = NY * TX * n2, L2 = TY * TX * n2;
+    if (guarded_out(guard, first_bad)) return;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    double* U = reinterpret_cast<double*>(smem_raw);
+    double* W = U + STAGES * C::U_D;
+    double* V = W + C::W_D;
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem_raw + C::SMEM_DATA);
+
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int q = lane & 3, g = lane >> 2;
+    const int M1 = (int)d.M1, M2 = (int)d.M2;
+    const int cx0 = blockIdx.x * TX, cy0 = blockIdx.y * TY;
+    const int64_t zc0 = d.z_begin + (int64_t)blockIdx.z * zchunk;
+    const int64_t zc1 = min(zc0 + (int64_t)zchunk, d.z_end);
+    const int P = (int)(zc1 - zc0) + 1;
+    const int64_t plane_elems = (int64_t)M1 * M2 * n3;
+
+    // B fragments: lane holds B[k = 4 ks + q][col = g] = A_axis[g][k] (zero for g >= n)
+    double bop[3][KS];
+#pragma unroll
+    for (int ax = 0; ax < 3; ++ax)
+#pragma unroll
+        for (int ks = 0; ks < KS; ++ks) bop[ax][ks] = g < n ? p.A[ax][g < n ? g : 0][4 * ks + q] : 0.0;
+
+    // loader: lane 0 of warp ly < NY copies tile row ly of every plane
+    int rowoff = 0, gx0 = 0;
+    if (tid == 0) {
+#pragma unroll
+        for (int s = 0; s < STAGES; ++s) mbar_init(&bars[s], 1);
+        mbar_fence_init();
+    }
+    if (lane == 0 && warp < NY) {
+        int gy = (cy0 + off + warp) % M2; if (gy < 0) gy += M2;
+        gx0 = (cx0 + off) % M1; if (gx0 < 0) gx0 += M1;
+        rowoff = gy * M1;
+    }
+    __syncthreads();
+    int64_t gz_next = d.periodic_z ? wrap(zc0 + off, d.M3) : zc0 + off;
+    int issued = 0;
+    auto issue = [&]() {
+        if (issued < P) {
+            if (lane == 0 && warp < NY) {
+                const int s = issued % STAGES;
+                fence_proxy_async_smem();
+                if (warp == 0) mbar_arrive_expect_tx(&bars[s], (unsigned)(C::NNODE * UNS * sizeof(double)));
+                const double* base = src + gz_next * plane_elems + (int64_t)rowoff * n3;
+                double* Ub = U + s * C::U_D + warp * NX * UNS;
+                int got = 0, gx = gx0;
+                while (got < NX) {
+                    const int len = min(NX - got, M1 - gx);
+                    bulk_g2s(Ub + got * UNS, base + (int64_t)gx * n3, (unsigned)(len * UNS * sizeof(double)), &bars[s]);
+                    got += len;
+                    gx = 0;
+                }
+            }
+            ++gz_next;
+            if (d.periodic_z && gz_next == d.M3) gz_next = 0;
+            ++issued;
+        }
+    };
+#pragma unroll
+    for (int s = 0; s < STAGES - 1; ++s) issue();
+
+    // Per-lane addressing, computed once: A-fragment input k = 4 ks + q -> (vertex a, component j);
+    // per pass and unrolled group iteration the lane's smem read/write offsets.  Lines past the
+    // end of a pass (ragged last group) read a clamped line and store nothing.
+    constexpr int I1 = (C::G1 + WARPS - 1) / WARPS, I2 = (C::G2 + WARPS - 1) / WARPS;
+    constexpr int I3 = (C::G3 + WARPS - 1) / WARPS;
+    int k1[KS], k2[KS], k3[KS], ka[KS];
+#pragma unroll
+    for (int ks = 0; ks < KS; ++ks) {
+        const int k = 4 * ks + q, a = k / n, j = k % n;
+        ka[ks] = a;
+        k1[ks] = a * UNS + j;      // x1: node cx + a along the row
+        k2[ks] = a * TX * WCS + j; // x2: cell row cy + a
+        k3[ks] = j * VJ;           // x3: V slot of plane p - 1 + a
+    }
+    const bool qout = 2 * q < n;  // this lane's output columns 2q, 2q + 1 are real outputs
+    int r1[I1], w1[I1], r2[I2], w2[I2], r3[I3], o3[I3];
+#pragma unroll
+    for (int it = 0; it < I1; ++it) {
+        const int l = (warp + WARPS * it) * 8 + g, lc = l < L1 ? l : L1 - 1;
+        const int rc = lc / n2, jj = lc - rc * n2, ly = rc / TX, cx = rc - ly * TX;  // rc = ly TX + cx
+        r1[it] = (ly * NX + cx) * UNS + jj * n;
+        w1[it] = (l < L1 && qout) ? rc * WCS + (2 * q) * WM + jj : -1;
+    }
+#pragma unroll
+    for (int it = 0; it < I2; ++it) {
+        const int l = (warp + WARPS * it) * 8 + g, lc = l < L2 ? l : L2 - 1;
+        const int cell = lc / n2, r = lc - cell * n2, j3 = r / n, m1 = r - j3 * n;
+        r2[it] = cell * WCS + m1 * WM + j3 * n;
+        w2[it] = (l < L2 && qout) ? cell * VCS + j3 * VJ + (2 * q) * n + m1 : -1;
+    }
+#pragma unroll
+    for (int it = 0; it < I3; ++it) {
+        const int l = (warp + WARPS * it) * 8 + g, lc = l < L2 ? l : L2 - 1;
+        const int cell = lc / n2, r = lc - cell * n2;
+        const int cx = cx0 + cell % TX, cy = cy0 + cell / TX;
+        r3[it] = cell * VCS + r;
+        // output offset within a node plane (int32: M1 M2 n^3 < 2^31 is checked at launch)
+        o3[it] = (l < L2 && qout && cx < M1 && cy < M2) ? (cy * M1 + cx) * n3 + (2 * q) * n2 + r : -1;
+    }
+
+    for (int pl = 0; pl < P; ++pl) {
+        __syncthreads();
+        issue();  // refills the stage read in iteration pl - 1
+        mbar_wait(&bars[pl % STAGES], (unsigned)((pl / STAGES) & 1));
+        const double* Ub = U + (pl % STAGES) * C::U_D;
+        double* Vc = V + (pl & 1) * C::V_D;
+
+        // ---- x1: line (ly TX + cx) n^2 + jj:  U(p) -> W ------------------------------------------
+        {
+            double d[I1][2];
+#pragma unroll
+            for (int it = 0; it < I1; ++it) {
+                d[it][0] = d[it][1] = 0.0;
+#pragma unroll
+                for (int ks = 0; ks < KS; ++ks) dmma(d[it][0], d[it][1], Ub[r1[it] + k1[ks]], bop[0][ks]);
+            }
+#pragma unroll
+            for (int it = 0; it < I1; ++it)
+                if (w1[it] >= 0) {
+                    W[w1[it]] = d[it][0];
+                    W[w1[it] + WM] = d[it][1];
+                }
+        }
+        __syncthreads();
+
+        // ---- x2: line cell n^2 + j3 n + m1:  W -> V[p & 1] ---------------------------------------
+        {
+            double d[I2][2];
+#pragma unroll
+            for (int it = 0; it < I2; ++it) {
+                d[it][0] = d[it][1] = 0.0;
+#pragma unroll
+                for (int ks = 0; ks < KS; ++ks) dmma(d[it][0], d[it][1], W[r2[it] + k2[ks]], bop[1][ks]);
+            }
+#pragma unroll
+            for (int it = 0; it < I2; ++it)
+                if (w2[it] >= 0) {
+                    Vc[w2[it]] = d[it][0];
+                    Vc[w2[it] + n] = d[it][1];
+                }
+        }
+        __syncthreads();
+
+        // ---- x3: line cell n^2 + (m2 n + m1), V planes p-1 and p -> dst (cell plane p-1) --------
+        if (pl > 0) {
+            const double* vk[KS];
+#pragma unroll
+            for (int ks = 0; ks < KS; ++ks) vk[ks] = V + ((pl - 1 + ka[ks]) & 1) * C::V_D + k3[ks];
+            double* oplane = dst + (zc0 + pl - 1) * plane_elems;
+            double d[I3][2];
+#pragma unroll
+            for (int it = 0; it < I3; ++it) {
+                d[it][0] = d[it][1] = 0.0;
+#pragma unroll
+                for (int ks = 0; ks < KS; ++ks) dmma(d[it][0], d[it][1], vk[ks][r3[it]], bop[2][ks]);
+            }
+#pragma unroll
+            for (int it = 0; it < I3; ++it)
+                if (o3[it] >= 0) {
+                    __stcs(oplane + o3[it], d[it][0]);
+                    __stcs(oplane + o3[it] + n2, d[it][1]);
+                    if (!isfinite(d[it][0]) || !isfinite(d[it][1]))
+                        flag_bad(first_bad, (zc0 + pl - 1) * M2 * (int64_t)M1 + o3[it] / n3);
+                }
+        }
+    }
+}
+
+template <class C>
+static int launch_cp(const double* src, double* dst, const Dims& d, const double* A, int off, cudaStream_t st,
+                     unsigned long long* first_bad, const unsigned long long* guard) {
+    const int64_t nz = d.z_end - d.z_begin;
+    if (nz <= 0) return 0;
+    if (d.M1 * d.M2 * C::n3 >= (int64_t(1) << 31)) return (int)cudaErrorInvalidValue;
+    SepOps<C::N> ops;
+    for (int k = 0; k < 3; ++k)
+        for (int m = 0; m < C::n; ++m)
+            for (int c = 0; c < 2 * C::n; ++c) {
+                ops.A[k][m][c] = A[(k * C::n + m) * 2 * C::n + c];
+                ops.Sh[k][m][c] = 0.0;
+            }
+    auto kern = sep_fused_dmma_cp_kernel<C>;
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM);
+    if (e != cudaSuccess) return (int)e;
+    const int64_t gx = (d.M1 + C::TX - 1) / C::TX, gy = (d.M2 + C::TY - 1) / C::TY;
+    const int64_t want = (int64_t)num_sms() * 4;
+    int64_t zsplit = (want + gx * gy - 1) / (gx * gy);
+    int64_t zchunk = (nz + zsplit - 1) / zsplit;
+    if (zchunk < 8) zchunk = nz < 8 ? nz : 8;
+    const int64_t gz = (nz + zchunk - 1) / zchunk;
+    kern<<<dim3((unsigned)gx, (unsigned)gy, (unsigned)gz), C::THREADS, C::SMEM, st>>>(src, dst, d, off, (int)zchunk,
+                                                                                   ops, first_bad, guard);
+    return (int)cudaGetLastError();
+}
+
+int sep_fused_dmma5_launch(const double* src, double* dst, const Dims& d, const double* A, int off, cudaStream_t st,
+                           unsigned long long* first_bad, const unsigned long long* guard) {
+    return launch_cp<cp5::Cfg<5, 4, 4>>(src, dst, d, A, off, st, first_bad, guard);
+}
+
+}  // namespace h3

@@ -288,7 +288,15 @@ int sep_fused_launch(const double* src, double* dst, const Dims& d, int order_n,
             return sep_fused_dmma3_launch(src, dst, d, A, off, st, first_bad, guard);
         }
         case 4: return sep_fused_n<4>(src, dst, d, A, off, st, first_bad, guard);
-        case 5: return sep_fused_n<5>(src, dst, d, A, off, st, first_bad, guard);
+        case 5: {
+            // FP64 tensor-core cell-pair kernel (h3_dmma5.cu) unless H3_FUSED_IMPL=dfma
+            static const bool use_dfma = [] {
+                const char* e = getenv("H3_FUSED_IMPL");
+                return e && strcmp(e, "dfma") == 0;
+            }();
+            if (use_dfma) return sep_fused_n<5>(src, dst, d, A, off, st, first_bad, guard);
+            return sep_fused_dmma5_launch(src, dst, d, A, off, st, first_bad, guard);
+        }
     }
     return (int)cudaErrorInvalidValue;
 }
