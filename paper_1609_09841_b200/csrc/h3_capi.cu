@@ -113,7 +113,7 @@ static int recon_impl(const T* src, T* coeff, int64_t M1, int64_t M2, int64_t M3
     }
     Dims d{M1, M2, M3, z_begin, z_end, periodic_z ? 1 : 0};
     if (fast && sizeof(T) == 8) {
-        // node-factorised reconstruction: FP64 tensor cores at N = 3, DFMA otherwise
+        // node-factorised reconstruction: FP64 tensor cores at N = 3 and 5, DFMA otherwise
         // (H3_RECON_IMPL=sep: DFMA kernel at N = 3 too; =fma: per-cell sweeps, for A/B runs)
         static const int impl = [] {
             const char* e = getenv("H3_RECON_IMPL");
@@ -124,6 +124,9 @@ static int recon_impl(const T* src, T* coeff, int64_t M1, int64_t M2, int64_t M3
         cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
         if (impl == 0 && order_n == 3)
             return h3::recon_dmma3_launch((const double*)src, (double*)coeff, d, (const double*)h_mat, off, st,
+                                          d_guard);
+        if (impl == 0 && order_n == 5)
+            return h3::recon_dmma5_launch((const double*)src, (double*)coeff, d, (const double*)h_mat, off, st,
                                           d_guard);
         if (impl != 2)
             return h3::recon_sep_launch((const double*)src, (double*)coeff, d, order_n, (const double*)h_mat, off,

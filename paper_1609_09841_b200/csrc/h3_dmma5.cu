@@ -290,4 +290,240 @@ int sep_fused_dmma5_launch(const double* src, double* dst, const Dims& d, const 
     return launch_cp<cp5::Cfg<5, 4, 4>>(src, dst, d, A, off, st, first_bad, guard);
 }
 
+// ---------------------------------------------------------------------------------------------
+// Reconstruction pass of the two-kernel step in the same cell-pair DMMA form (N = 5):
+//   coeff(c) = sum_a (H^a3 (x) H^a2 (x) H^a1) u(c + off + a),  H^a = H[:, a n : a n + n],
+// a pass line gathers its cell's two vertex blocks (K = 2n = 12) and produces s = 12 outputs
+// (two 8-column blocks, 12 of 16 used).  H is the same for all three axes, so the whole operator
+// is 6 registers per lane.  x3 writes the (2N+2)^3 coefficient block of each cell straight to HBM
+// (the two-kernel intermediate, gridkernels.py:142-160 layout [i3][i2][i1]).
+// ---------------------------------------------------------------------------------------------
+namespace rcp {
+template <int N_, int TX_, int TY_, int STAGES_>
+struct Cfg {
+    static constexpr int N = N_, n = N + 1, n2 = n * n, n3 = n2 * n, S = 2 * n, S2 = S * S, S3 = S2 * S;
+    static constexpr int KS = S / 4, CB = (S + 7) / 8;  // k-steps, 8-column output blocks
+    static_assert(S % 4 == 0, "cell-pair form needs 2n divisible by 4");
+    static constexpr int TX = TX_, TY = TY_, NX = TX + 1, NY = TY + 1, NNODE = NX * NY;
+    static constexpr int WARPS = 16, THREADS = 32 * WARPS, STAGES = STAGES_;
+    static constexpr int UNS = n3;
+    static constexpr int WI = n2 + 1, WCS = S * WI;  // W: [node row][cell][i1][j3 j2]
+    static constexpr int VJ = S2 + 1, VCS = n * VJ;  // V: [cell][j3][i2 i1]
+    static constexpr int L1 = NY * TX * n2, L2 = TY * TX * n * S, L3 = TY * TX * S2;
+    static constexpr int G1 = (L1 + 7) / 8, G2 = (L2 + 7) / 8, G3 = (L3 + 7) / 8;
+    static constexpr size_t U_D = (size_t)NNODE * UNS;
+    static constexpr size_t W_D = (size_t)NY * TX * WCS;
+    static constexpr size_t V_D = (size_t)TY * TX * VCS;
+    static constexpr size_t SMEM_DATA = (STAGES * U_D + W_D + 2 * V_D) * sizeof(double);
+    static constexpr size_t SMEM = SMEM_DATA + STAGES * sizeof(uint64_t);
+    static_assert(NY <= WARPS, "one loader warp per tile row");
+};
+}  // namespace rcp
+
+template <class C>
+__global__ void __launch_bounds__(C::THREADS, 1)
+recon_dmma_cp_kernel(const double* __restrict__ src, double* __restrict__ coeff, Dims d, int off, int zchunk,
+                     const __grid_constant__ LitOps<double, C::N> hp, const unsigned long long* guard) {
+    using namespace cp5;
+    constexpr int n = C::n, n2 = C::n2, n3 = C::n3, S = C::S, S2 = C::S2, S3 = C::S3, KS = C::KS, CB = C::CB;
+    constexpr int TX = C::TX, NX = C::NX, NY = C::NY, WARPS = C::WARPS, STAGES = C::STAGES, UNS = C::UNS;
+    constexpr int WI = C::WI, WCS = C::WCS, VJ = C::VJ, VCS = C::VCS, L1 = C::L1, L2 = C::L2, L3 = C::L3;
+    constexpr int I1 = (C::G1 + WARPS - 1) / WARPS, I2 = (C::G2 + WARPS - 1) / WARPS;
+    constexpr int I3 = (C::G3 + WARPS - 1) / WARPS;
+    if (guarded_out(guard, nullptr)) return;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    double* U = reinterpret_cast<double*>(smem_raw);
+    double* W = U + STAGES * C::U_D;
+    double* V = W + C::W_D;
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem_raw + C::SMEM_DATA);
+
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int q = lane & 3, g = lane >> 2;
+    const int M1 = (int)d.M1, M2 = (int)d.M2;
+    const int cx0 = blockIdx.x * TX, cy0 = blockIdx.y * C::TY;
+    const int64_t zc0 = d.z_begin + (int64_t)blockIdx.z * zchunk;
+    const int64_t zc1 = min(zc0 + (int64_t)zchunk, d.z_end);
+    const int P = (int)(zc1 - zc0) + 1;
+    const int64_t plane_elems = (int64_t)M1 * M2 * n3;
+    const int64_t cplane = (int64_t)M1 * M2 * S3;
+
+    // B fragments (all axes): lane holds B[k = 4 ks + q][col = 8 cb + g] = H[8 cb + g][k]
+    double bop[KS][CB];
+#pragma unroll
+    for (int ks = 0; ks < KS; ++ks)
+#pragma unroll
+        for (int cb = 0; cb < CB; ++cb) {
+            const int col = 8 * cb + g;
+            bop[ks][cb] = col < S ? hp.H[(col < S ? col : 0) * S + 4 * ks + q] : 0.0;
+        }
+
+    int rowoff = 0, gx0 = 0;
+    if (tid == 0) {
+#pragma unroll
+        for (int s = 0; s < STAGES; ++s) mbar_init(&bars[s], 1);
+        mbar_fence_init();
+    }
+    if (lane == 0 && warp < NY) {
+        int gy = (cy0 + off + warp) % M2; if (gy < 0) gy += M2;
+        gx0 = (cx0 + off) % M1; if (gx0 < 0) gx0 += M1;
+        rowoff = gy * M1;
+    }
+    __syncthreads();
+    int64_t gz_next = d.periodic_z ? wrap(zc0 + off, d.M3) : zc0 + off;
+    int issued = 0;
+    auto issue = [&]() {
+        if (issued < P) {
+            if (lane == 0 && warp < NY) {
+                const int s = issued % STAGES;
+                fence_proxy_async_smem();
+                if (warp == 0) mbar_arrive_expect_tx(&bars[s], (unsigned)(C::NNODE * UNS * sizeof(double)));
+                const double* base = src + gz_next * plane_elems + (int64_t)rowoff * n3;
+                double* Ub = U + s * C::U_D + warp * NX * UNS;
+                int got = 0, gx = gx0;
+                while (got < NX) {
+                    const int len = min(NX - got, M1 - gx);
+                    bulk_g2s(Ub + got * UNS, base + (int64_t)gx * n3, (unsigned)(len * UNS * sizeof(double)), &bars[s]);
+                    got += len;
+                    gx = 0;
+                }
+            }
+            ++gz_next;
+            if (d.periodic_z && gz_next == d.M3) gz_next = 0;
+            ++issued;
+        }
+    };
+#pragma unroll
+    for (int s = 0; s < STAGES - 1; ++s) issue();
+
+    int k1[KS], k2[KS], k3[KS], ka[KS];
+#pragma unroll
+    for (int ks = 0; ks < KS; ++ks) {
+        const int k = 4 * ks + q, a = k / n, j = k % n;
+        ka[ks] = a;
+        k1[ks] = a * UNS + j;
+        k2[ks] = a * TX * WCS + j;
+        k3[ks] = j * VJ;
+    }
+    // output columns of this lane: 8 cb + 2q (+1); the last block is partial when S % 8 != 0
+    const bool cout1 = 8 * (CB - 1) + 2 * q < S;
+    int r1[I1], w1[I1], r2[I2], w2[I2], r3[I3], o3[I3];
+#pragma unroll
+    for (int it = 0; it < I1; ++it) {
+        const int l = (warp + WARPS * it) * 8 + g, lc = l < L1 ? l : L1 - 1;
+        const int rc = lc / n2, jj = lc - rc * n2, ly = rc / TX, cx = rc - ly * TX;
+        r1[it] = (ly * NX + cx) * UNS + jj * n;
+        w1[it] = l < L1 ? rc * WCS + (2 * q) * WI + jj : -1;  // + 8 cb WI
+    }
+#pragma unroll
+    for (int it = 0; it < I2; ++it) {
+        const int l = (warp + WARPS * it) * 8 + g, lc = l < L2 ? l : L2 - 1;
+        const int cell = lc / (n * S), r = lc - cell * (n * S), j3 = r / S, i1 = r - j3 * S;
+        r2[it] = cell * WCS + i1 * WI + j3 * n;
+        w2[it] = l < L2 ? cell * VCS + j3 * VJ + (2 * q) * S + i1 : -1;  // + 8 cb S
+    }
+#pragma unroll
+    for (int it = 0; it < I3; ++it) {
+        const int l = (warp + WARPS * it) * 8 + g, lc = l < L3 ? l : L3 - 1;
+        const int cell = lc / S2, r = lc - cell * S2;
+        const int cx = cx0 + cell % TX, cy = cy0 + cell / C::TX;
+        r3[it] = cell * VCS + r;
+        o3[it] = (l < L3 && cx < M1 && cy < M2) ? (cy * M1 + cx) * S3 + (2 * q) * S2 + r : -1;  // + 8 cb S2
+    }
+
+    for (int pl = 0; pl < P; ++pl) {
+        __syncthreads();
+        issue();
+        mbar_wait(&bars[pl % STAGES], (unsigned)((pl / STAGES) & 1));
+        const double* Ub = U + (pl % STAGES) * C::U_D;
+        double* Vc = V + (pl & 1) * C::V_D;
+
+        // ---- x1: U(p) -> W[row][cell][i1][j3 j2] ----------------------------------------------
+#pragma unroll
+        for (int it = 0; it < I1; ++it) {
+            double a[KS];
+#pragma unroll
+            for (int ks = 0; ks < KS; ++ks) a[ks] = Ub[r1[it] + k1[ks]];
+#pragma unroll
+            for (int cb = 0; cb < CB; ++cb) {
+                double d0 = 0.0, d1 = 0.0;
+#pragma unroll
+                for (int ks = 0; ks < KS; ++ks) dmma(d0, d1, a[ks], bop[ks][cb]);
+                if (w1[it] >= 0 && (cb < CB - 1 || cout1)) {
+                    W[w1[it] + 8 * cb * WI] = d0;
+                    W[w1[it] + (8 * cb + 1) * WI] = d1;
+                }
+            }
+        }
+        __syncthreads();
+
+        // ---- x2: W -> V[p & 1][cell][j3][i2 i1] -------------------------------------------------
+#pragma unroll
+        for (int it = 0; it < I2; ++it) {
+            double a[KS];
+#pragma unroll
+            for (int ks = 0; ks < KS; ++ks) a[ks] = W[r2[it] + k2[ks]];
+#pragma unroll
+            for (int cb = 0; cb < CB; ++cb) {
+                double d0 = 0.0, d1 = 0.0;
+#pragma unroll
+                for (int ks = 0; ks < KS; ++ks) dmma(d0, d1, a[ks], bop[ks][cb]);
+                if (w2[it] >= 0 && (cb < CB - 1 || cout1)) {
+                    Vc[w2[it] + 8 * cb * S] = d0;
+                    Vc[w2[it] + (8 * cb + 1) * S] = d1;
+                }
+            }
+        }
+        __syncthreads();
+
+        // ---- x3: V planes p-1, p -> coeff (cell plane p-1), streaming stores ------------------
+        if (pl > 0) {
+            const double* vk[KS];
+#pragma unroll
+            for (int ks = 0; ks < KS; ++ks) vk[ks] = V + ((pl - 1 + ka[ks]) & 1) * C::V_D + k3[ks];
+            double* oplane = coeff + (zc0 - d.z_begin + pl - 1) * cplane;
+#pragma unroll
+            for (int it = 0; it < I3; ++it) {
+                double a[KS];
+#pragma unroll
+                for (int ks = 0; ks < KS; ++ks) a[ks] = vk[ks][r3[it]];
+#pragma unroll
+                for (int cb = 0; cb < CB; ++cb) {
+                    double d0 = 0.0, d1 = 0.0;
+#pragma unroll
+                    for (int ks = 0; ks < KS; ++ks) dmma(d0, d1, a[ks], bop[ks][cb]);
+                    if (o3[it] >= 0 && (cb < CB - 1 || cout1)) {
+                        __stcs(oplane + o3[it] + 8 * cb * S2, d0);
+                        __stcs(oplane + o3[it] + (8 * cb + 1) * S2, d1);
+                    }
+                }
+            }
+        }
+    }
+}
+
+int recon_dmma5_launch(const double* src, double* coeff, const Dims& d, const double* h_mat, int off,
+                       cudaStream_t st, const unsigned long long* guard) {
+    using C = rcp::Cfg<5, 4, 2, 2>;
+    const int64_t nz = d.z_end - d.z_begin;
+    if (nz <= 0) return 0;
+    if (d.M1 * d.M2 * C::S3 >= (int64_t(1) << 31)) return (int)cudaErrorInvalidValue;  // int32 plane offsets
+    LitOps<double, 5> hp;
+    for (int i = 0; i < C::S2; ++i) hp.H[i] = h_mat[i];
+    for (int i = 0; i < C::S; ++i) hp.f1[i] = hp.f2[i] = hp.f3[i] = 0.0;
+    for (int i = 0; i < H3_MAX_STAGES; ++i) hp.cf[i] = 0.0;
+    hp.q = 0;
+    auto kern = recon_dmma_cp_kernel<C>;
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM);
+    if (e != cudaSuccess) return (int)e;
+    const int64_t gx = (d.M1 + C::TX - 1) / C::TX, gy = (d.M2 + C::TY - 1) / C::TY;
+    const int64_t want = (int64_t)num_sms() * 4;
+    int64_t zsplit = (want + gx * gy - 1) / (gx * gy);
+    int64_t zchunk = (nz + zsplit - 1) / zsplit;
+    if (zchunk < 8) zchunk = nz < 8 ? nz : 8;
+    const int64_t gz = (nz + zchunk - 1) / zchunk;
+    kern<<<dim3((unsigned)gx, (unsigned)gy, (unsigned)gz), C::THREADS, C::SMEM, st>>>(src, coeff, d, off, (int)zchunk,
+                                                                                   hp, guard);
+    return (int)cudaGetLastError();
+}
+
 }  // namespace h3

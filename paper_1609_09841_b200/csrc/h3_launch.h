@@ -59,6 +59,8 @@ int sep_fused_dmma3_launch(const double* src, double* dst, const Dims& d, const 
 int sep_fused_dmma5_launch(const double* src, double* dst, const Dims& d, const double* A, int off,
                            cudaStream_t st, unsigned long long* first_bad,
                            const unsigned long long* guard);
+int recon_dmma5_launch(const double* src, double* coeff, const Dims& d, const double* h_mat, int off,
+                       cudaStream_t st, const unsigned long long* guard);
 int recon_dmma3_launch(const double* src, double* coeff, const Dims& d, const double* h_mat, int off,
                        cudaStream_t st, const unsigned long long* guard);
 int recon_sep_launch(const double* src, double* coeff, const Dims& d, int order_n, const double* h_mat,
