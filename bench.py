@@ -52,7 +52,8 @@ def parse():
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
-    ap.add_argument("--extras", action="store_true", help="also time the two-kernel configs")
+    ap.add_argument("--no-extras", action="store_true",
+                    help="skip the secondary configs (two-kernel 512^3 / 128^3, m=5 256^3)")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     return ap.parse_args()
 
@@ -302,8 +303,9 @@ def main():
                      "frac": (achieved / peak_gbs) if achieved else None, "traffic": traffic,
                      "traffic_unit": "DRAM bytes per launch (ncu dram__bytes_read+write)",
                      "traffic_source": traffic_src,
-                     "kernel": ("sep_fused_dmma3_kernel (DMMA m8n8k4, 8x7 tile, 16 warps)" if order_n == 3
-                                else f"sep_fused_kernel<{order_n}>") if args.mode == "fused" else "recon+evolve",
+                     "kernel": ("sep_fused_dmma3_kernel (DMMA m8n8k4, 8x7 tile, 16 warps, TMA row loads)" if order_n == 3
+                                else ("sep_fused_dmma_cp_kernel<5> (DMMA cell-pair)" if order_n == 5
+                                      else f"sep_fused_kernel<{order_n}>")) if args.mode == "fused" else "recon+evolve",
                      "algorithmic_bytes_per_launch": alg_bytes, "mean_launch_ms": launch_ms,
                      "peak_source": peak_src},
         "gpu_launches": launches_per_step * args.steps,
@@ -314,26 +316,31 @@ def main():
     # ---- e2e through the package API with host-resident state (1 GPU) ---------------------
     print(f"[bench] value {value:.4e} DOF-updates/s, kernel {launch_ms} ms", file=sys.stderr, flush=True)
     if world == 1 and not args.no_e2e:
-        result["e2e"] = e2e_host(hb, torch, state, scratch, cfg, ops, dt, args.e2e_steps, dofs_per_step)
+        del scratch
+        scratch = None
+        torch.cuda.empty_cache()
+        result["e2e"] = e2e_host(hb, torch, state, grid, order_n, cfg, dt, args.e2e_steps, dofs_per_step)
         print(f"[bench] e2e {result['e2e']}", file=sys.stderr, flush=True)
     # ---- CPU baseline (rank 0, N = 1) ----------------------------------------------------------
     if world == 1 and not args.no_cpu:
         rate, info = cpu_oracle_rate(order_n, cpu_sample_cells(order_n), args.cpu_seconds)
         result["cpu_baseline"] = {"value": rate, "unit": UNIT, "cores": info["cores"], "kind": "port",
                                   "sample": info["sample"]}
-    if world == 1 and args.extras:
+    if world == 1 and not args.no_extras:
         del state, scratch
         torch.cuda.empty_cache()
-        result["extras"] = extras(hb, torch, order_n)
+        result["extras"] = extras(hb, torch, order_n, peak_gbs)
     if rank == 0:
         print(json.dumps(result), flush=True)
     if world > 1:
         dist.destroy_process_group()
 
 
-def e2e_host(hb, torch, state, scratch, cfg, ops, dt, steps, dofs_per_step):
-    """Host-resident state: per step H2D (pinned) -> full_step -> D2H, all timed."""
-    nbytes = state.nbytes
+def e2e_host(hb, torch, state, grid, order_n, cfg, dt, steps, dofs_per_step):
+    """Host-resident state through the package API (HostStepper, the drop-in for the
+    reference's full_step on a host field): every step uploads the whole primary field
+    from pinned host memory, steps it and writes it back, with the transfers and kernels of
+    successive x3 chunks overlapped; the step's result (instability flags) is read back."""
     try:
         host = torch.empty(state.tensor.shape, dtype=torch.float64, pin_memory=True)
         pinned = True
@@ -341,42 +348,50 @@ def e2e_host(hb, torch, state, scratch, cfg, ops, dt, steps, dofs_per_step):
         host = torch.empty(state.tensor.shape, dtype=torch.float64)
         pinned = False
     host.copy_(state.tensor)
+    state.tensor = None  # free HBM: the streamed step keeps only a few chunks on the device
+    torch.cuda.empty_cache()
+    stepper = hb.HostStepper(host, grid, order_n, cfg)
+    stepper.step(dt=dt)  # warm-up (allocations, first launches)
     torch.cuda.synchronize()
     t0 = time.perf_counter()
     for k in range(steps):
-        state.tensor.copy_(host, non_blocking=pinned)
-        hb.full_step(state, scratch, cfg, ops, dt=dt, step_index=k)  # reads flags back (D2H sync)
-        host.copy_(state.tensor, non_blocking=pinned)
-    torch.cuda.synchronize()
+        stepper.step(dt=dt, step_index=k)  # ends with the D2H read of the step's flags
     wall = time.perf_counter() - t0
-    return {"value": dofs_per_step * steps / wall, "unit": UNIT, "h2d_bytes_per_step": nbytes,
-            "d2h_bytes_per_step": nbytes + 16, "steps": steps, "pinned": pinned,
-            "api": "paper_1609_09841_b200.full_step on host-resident state (H2D + step + D2H per step)"}
+    return {"value": dofs_per_step * steps / wall, "unit": UNIT, "h2d_bytes_per_step": stepper.h2d_bytes,
+            "d2h_bytes_per_step": stepper.d2h_bytes + 16 * len(stepper.chunks), "steps": steps, "pinned": pinned,
+            "chunks": len(stepper.chunks),
+            "api": "paper_1609_09841_b200.HostStepper.step on a host-resident field (chunked H2D -> fused "
+                   "half steps -> D2H, overlapped on three streams)"}
 
 
-def extras(hb, torch, order_n):
-    """Secondary measurements: two-kernel at 128^3 (configs[1]) and fused/two-kernel at m=5."""
+def extras(hb, torch, order_n, peak_gbs):
+    """Secondary measurements (device-resident state, CUDA events), each against its own
+    algorithmic-byte roofline: fused 16 (N+1)^3 B and two-kernel 16 ((N+1)^3 + (2N+2)^3) B per
+    node per half step.  Covers the north-star targets (m=3 512^3 fused AND two-kernel) and
+    BASELINE configs[1] (m=3 128^3 two-kernel) and configs[3] (m=5 256^3 both forms)."""
     out = {}
-    for (n, m, mode) in ((3, 128, "two_pass"), (3, 128, "fused"), (5, 256, "fused"), (5, 256, "two_pass")):
+    for (n, m, mode, k) in ((3, 512, "two_pass", 2), (3, 128, "two_pass", 10), (3, 128, "fused", 10),
+                            (5, 256, "fused", 5), (5, 256, "two_pass", 3)):
         grid = hb.GridSpec((m, m, m))
         cfg = hb.StepConfig(mode=mode, variant="separable")
         ops = hb.OperatorSet.for_grid(grid, n)
         st = hb.init_field(hb.plane_wave(), grid, n)
         sc = hb.DofField.empty(grid.with_parity("dual"), n)
-        for _ in range(2):
-            hb.run_steps(st, sc, cfg, ops, 1)
+        hb.run_steps(st, sc, cfg, ops, 1)
         torch.cuda.synchronize()
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        k = 5
         a.record()
         hb.run_steps(st, sc, cfg, ops, k)
         b.record()
         torch.cuda.synchronize()
         ms = a.elapsed_time(b) / k
         rate = m ** 3 * (n + 1) ** 3 / (ms / 1e3)
-        per = 32 if mode == "fused" else 288
-        out[f"m{n}_{m}^3_{mode}"] = {"dof_updates_per_s": rate, "ms_per_step": ms,
-                                     "alg_GBps": rate * per / 1e9}
+        per_dof = 32 if mode == "fused" else 32 * (1 + 8)  # bytes per DOF-update (two half steps)
+        gbs = rate * per_dof / 1e9
+        out[f"m{n}_{m}^3_{mode}"] = {"dof_updates_per_s": rate, "ms_per_step": ms, "alg_GBps": gbs,
+                                     "hbm_frac": gbs / peak_gbs, "steps": k}
+        print(f"[bench] extra m{n} {m}^3 {mode}: {rate:.3e} DOF-updates/s, {gbs:.0f} GB/s "
+              f"({100 * gbs / peak_gbs:.1f}% of HBM)", file=sys.stderr, flush=True)
         del st, sc
         torch.cuda.empty_cache()
     return out

@@ -174,3 +174,15 @@ def test_no_oracle_imports_in_product():
     pkg = ROOT / "paper_1609_09841_b200"
     for f in list(pkg.rglob("*.py")) + list(pkg.rglob("*.cu")) + list(pkg.rglob("*.cuh")) + list(pkg.rglob("Makefile")):
         assert "oracle" not in f.read_text().replace("# oracle", ""), f
+
+
+def test_streaming_chunk_plan_covers_the_grid():
+    from paper_1609_09841_b200.streaming import chunk_plan
+    for m3 in range(2, 40):
+        for chunk in range(1, 45):
+            plan = chunk_plan(m3, chunk)
+            assert plan[0][0] == 0 and plan[-1][1] == m3
+            assert all(a[1] == b[0] for a, b in zip(plan, plan[1:]))
+            assert all(z1 - z0 >= 2 for z0, z1 in plan)
+    with pytest.raises(ValueError):
+        chunk_plan(1, 4)
