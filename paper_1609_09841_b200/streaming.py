@@ -72,8 +72,8 @@ class HostStepper:
         self.device = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
         self.ops = OperatorSet.for_grid(self.grid, order_n)
         plane = m1 * m2 * n ** 3
-        if chunk_planes is None:  # ~4 GB chunks: large copies, a few chunks of HBM in flight
-            chunk_planes = max(2, (4 << 30) // (plane * 8))
+        if chunk_planes is None:  # ~2 GB chunks: measured best at 512^3 (tools/time_stream.py)
+            chunk_planes = max(2, (2 << 30) // (plane * 8))
         self.chunks = chunk_plan(m3, chunk_planes)
         cmax = max(z1 - z0 for z0, z1 in self.chunks)
         kw = dict(dtype=torch.float64, device=self.device)
