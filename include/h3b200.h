@@ -16,7 +16,11 @@
  *   - src/dst/coeff and every d_* pointer are DEVICE pointers; h_mat, fac*,
  *     cfac are HOST arrays (tiny, copied into kernel parameters per call).
  *   - All calls are asynchronous on `stream` (a cudaStream_t; NULL = legacy
- *     default stream), reentrant, and keep no mutable global state.
+ *     default stream) and reentrant.  The only process-wide state is a small
+ *     constant-memory ring holding the DFMA kernels' operators; it is
+ *     mutex-protected and a slot is rewritten only after every kernel that
+ *     used it has completed (stream events), so concurrent calls on different
+ *     streams with different operators are safe.
  *   - Return 0 on success, a positive cudaError_t on a CUDA error, or a
  *     negative H3_ERR_* code for invalid arguments.  No C++ exception crosses
  *     the ABI.
@@ -71,7 +75,8 @@ int h3_fused_pass_f32(const float* src, float* dst, int64_t M1, int64_t M2, int6
 /* Replaces gridkernels.recon_pass(src, coeff, h_mat, tiles, off) (gridkernels.py:142-160;
  * pipeline.py:262).  coeff holds only the cells [z_begin, z_end) (slab chunk):
  * coeff[(c3 - z_begin)][c2][c1][s][s][s].  variant LITERAL = reference summation
- * order without FMA; SEPARABLE/AUTO = same sweeps with FMA. */
+ * order without FMA (bit-identical); SEPARABLE/AUTO = the same tensor computed
+ * node-factorised (FP64 tensor cores at N = 3, 5; constant-operand DFMA otherwise). */
 int h3_recon_pass(const double* src, double* coeff, int64_t M1, int64_t M2, int64_t M3,
                   int order_n, const double* h_mat, int off, int64_t z_begin, int64_t z_end,
                   int periodic_z, int variant, void* stream, const unsigned long long* d_guard);
