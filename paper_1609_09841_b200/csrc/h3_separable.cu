@@ -315,7 +315,7 @@ int sep_fused_launch(const double* src, double* dst, const Dims& d, int order_n,
 template <int N>
 constexpr int ev_cpb() { return (2 * N + 2) * (2 * N + 2) >= 256 ? 1 : 256 / ((2 * N + 2) * (2 * N + 2)); }
 
-template <int N, int CPB>
+template <int N, int CPB, int GPC>
 __global__ void __launch_bounds__(CPB*(2 * N + 2) * (2 * N + 2))
 sep_evolve_kernel(const double* __restrict__ coeff, double* __restrict__ dst, Dims d,
                   const __grid_constant__ SepOps<N> p, unsigned long long* first_bad,
@@ -324,7 +324,6 @@ sep_evolve_kernel(const double* __restrict__ coeff, double* __restrict__ dst, Di
     constexpr int THREADS = CPB * S2;
     constexpr int T1S = S2 * n + 1;  // per-cell stride of the pass-x1 output (odd: spreads banks)
     constexpr int T2S = S * n2 + 1;
-    if (guarded_out(guard, first_bad)) return;
     __shared__ double T1[CPB * T1S];  // [c][i3][i2][m1]
     __shared__ double T2[CPB * T2S];  // [c][i3][m2][m1]
 
@@ -334,31 +333,38 @@ sep_evolve_kernel(const double* __restrict__ coeff, double* __restrict__ dst, Di
     const int tid = threadIdx.x;
     const int c = tid / S2, line = tid - (tid / S2) * S2;  // x1 task: (cell, line (i3, i2))
 
-    double u[S];
-    auto load = [&](int64_t grp) {
+    // GPC consecutive groups per CTA, all loads issued up front (the later groups' loads are
+    // in flight while the earlier ones are contracted), then the guard read (overlapped too)
+    double u[GPC][S];
+#pragma unroll
+    for (int gi = 0; gi < GPC; ++gi) {
+        const int64_t grp = (int64_t)blockIdx.x * GPC + gi;
         const int64_t cell = grp * CPB + c;
         if (grp < groups && cell < total) {
             const double2* g2 = reinterpret_cast<const double2*>(coeff + cell * S3 + line * S);
 #pragma unroll
             for (int k = 0; k < S / 2; ++k) {
                 const double2 v = __ldcs(g2 + k);
-                u[2 * k] = v.x;
-                u[2 * k + 1] = v.y;
+                u[gi][2 * k] = v.x;
+                u[gi][2 * k + 1] = v.y;
             }
         } else {
 #pragma unroll
-            for (int k = 0; k < S; ++k) u[k] = 0.0;
+            for (int k = 0; k < S; ++k) u[gi][k] = 0.0;
         }
-    };
-    const int64_t grp = blockIdx.x;
-    load(grp);
-    {
+    }
+    if (guarded_out(guard, first_bad)) return;
+#pragma unroll
+    for (int gi = 0; gi < GPC; ++gi) {
+        const int64_t grp = (int64_t)blockIdx.x * GPC + gi;
+        if (grp >= groups) break;
+        if (gi > 0) __syncthreads();  // T1/T2 reuse
         // pass x1 (registers): T1[c][i3][i2][m1] = sum_i1 S1[m1][i1] u[i1]
 #pragma unroll
         for (int m = 0; m < n; ++m) {
-            double acc = p.Sh[0][m][0] * u[0];
+            double acc = p.Sh[0][m][0] * u[gi][0];
 #pragma unroll
-            for (int k = 1; k < S; ++k) acc = fma(p.Sh[0][m][k], u[k], acc);
+            for (int k = 1; k < S; ++k) acc = fma(p.Sh[0][m][k], u[gi][k], acc);
             T1[c * T1S + line * n + m] = acc;
         }
         __syncthreads();
@@ -399,11 +405,10 @@ sep_evolve_kernel(const double* __restrict__ coeff, double* __restrict__ dst, Di
             }
             if (bad) flag_bad(first_bad, node);
         }
-        __syncthreads();
     }
 }
 
-template <int N, int CPB>
+template <int N, int CPB, int GPC = 1>
 static int sep_evolve_nc(const double* coeff, double* dst, const Dims& d, const double* Sh,
                         cudaStream_t st, unsigned long long* first_bad,
                         const unsigned long long* guard) {
@@ -417,9 +422,9 @@ static int sep_evolve_nc(const double* coeff, double* dst, const Dims& d, const 
                 ops.Sh[k][m][c] = Sh[(k * n + m) * S + c];
                 ops.A[k][m][c] = 0.0;
             }
-    auto kern = sep_evolve_kernel<N, CPB>;
+    auto kern = sep_evolve_kernel<N, CPB, GPC>;
     const int64_t groups = (total + CPB - 1) / CPB;
-    kern<<<(unsigned)groups, CPB * S2, 0, st>>>(coeff, dst, d, ops, first_bad, guard);
+    kern<<<(unsigned)((groups + GPC - 1) / GPC), CPB * S2, 0, st>>>(coeff, dst, d, ops, first_bad, guard);
     return (int)cudaGetLastError();
 }
 
@@ -434,6 +439,7 @@ static int sep_evolve_n(const double* coeff, double* dst, const Dims& d, const d
         }();
         if (cpb == 4) return sep_evolve_nc<3, 4>(coeff, dst, d, Sh, st, first_bad, guard);
         if (cpb == 2) return sep_evolve_nc<3, 2>(coeff, dst, d, Sh, st, first_bad, guard);
+        if (cpb == 42) return sep_evolve_nc<3, 4, 2>(coeff, dst, d, Sh, st, first_bad, guard);
         return sep_evolve_nc<3, 8>(coeff, dst, d, Sh, st, first_bad, guard);
     }
     return sep_evolve_nc<N, ev_cpb<N>()>(coeff, dst, d, Sh, st, first_bad, guard);
