@@ -84,10 +84,15 @@ __device__ __forceinline__ void fence_proxy_async_smem() {
 // of 16-B cp.async by every thread (which cost ~50 address instructions per warp per plane).
 // ABL (measurement-only ablations, results are garbage): bit 0 skips the global stores,
 // bit 1 the input copies, bit 2 replaces every DMMA by a register update.
-template <int TY_, int WARPS_, int STAGES_, bool VALIAS_, int MINB_ = 1, int ABL_ = 0, bool TMA_ = false>
+template <int TY_, int WARPS_, int STAGES_, bool VALIAS_, int MINB_ = 1, int ABL_ = 0, bool TMA_ = false,
+          bool LEAN_ = false>
 struct Dm3Cfg {
     static constexpr int ABL = ABL_;
     static constexpr bool TMA = TMA_;
+    // LEAN: x3 stores each chain's finished lanes with predicated half-warp stores at 32-bit
+    // offsets from a per-plane base, and screens for non-finite values with one integer min
+    // per value (the exact node is located on a rare path).
+    static constexpr bool LEAN = LEAN_;
     static constexpr int MINB = MINB_;  // CTAs per SM the register budget is sized for
     static constexpr int n = 4, n3 = 64;
     static constexpr int TX = 8, TY = TY_, NX = TX + 1, NY = TY + 1, NCOL = NX * NY;
@@ -234,6 +239,17 @@ sep_fused_dmma3_kernel(const double* __restrict__ src, double* __restrict__ dst,
                        ? ((zc0 * M2 + cy) * (int64_t)M1 + cx) * n3 + (2 * (q & 1)) * 16 + 8 * h + g
                        : -1;
     }
+    // LEAN: the lane's output offset within a node plane (int32; M1 M2 64 < 2^31 checked at launch)
+    int ooff[C::LEAN ? K3 : 1];
+    if constexpr (C::LEAN) {
+#pragma unroll
+        for (int k = 0; k < K3; ++k) {
+            const int t = warp + WARPS * k;
+            const int cell = t >> 1, h = t & 1;
+            const int cx = cx0 + (cell % TX), cy = cy0 + cell / TX;
+            ooff[k] = (cx < M1 && cy < M2) ? (cy * M1 + cx) * n3 + (2 * (q & 1)) * 16 + 8 * h + g : -1;
+        }
+    }
     double acc[K3][2];
 #pragma unroll
     for (int k = 0; k < K3; ++k) acc[k][0] = acc[k][1] = 0.0;
@@ -367,7 +383,32 @@ sep_fused_dmma3_kernel(const double* __restrict__ src, double* __restrict__ dst,
                 acc[k][0] = done ? 0.0 : acc[k][0];
                 acc[k][1] = done ? 0.0 : acc[k][1];
             }
-            if (pl > 0) {
+            if constexpr (C::LEAN) {
+                if (pl > 0) {
+                    double* oplane = dst + (zc0 + pl - 1) * plane_elems;
+                    unsigned screen = 0x7ff00000u;
+#pragma unroll
+                    for (int k = 0; k < K3; ++k) {
+                        const bool done = par == ((pl + k + 1) & 1);
+                        if (done && ooff[k] >= 0) {
+                            if (!(C::ABL & 1)) {
+                                __stcs(oplane + ooff[k], v0[k]);
+                                __stcs(oplane + ooff[k] + 16, v1[k]);
+                            }
+                        }
+                        screen = min(screen, min(~(unsigned)__double2hiint(v0[k]) & 0x7ff00000u,
+                                                 ~(unsigned)__double2hiint(v1[k]) & 0x7ff00000u));
+                    }
+                    if (screen == 0u) {  // rare: some lane holds Inf/NaN (finished or partial)
+#pragma unroll
+                        for (int k = 0; k < K3; ++k) {
+                            const bool done = par == ((pl + k + 1) & 1);
+                            if (done && ooff[k] >= 0 && (!isfinite(v0[k]) || !isfinite(v1[k])))
+                                flag_bad(first_bad, (zc0 + pl - 1) * M2 * (int64_t)M1 + ooff[k] / n3);
+                        }
+                    }
+                }
+            } else if (pl > 0) {
 #pragma unroll
                 for (int k = 0; k < K3; k += 2) {
                     // lanes with par == ((pl + k + 1) & 1) hold chain k, the others chain k+1
@@ -749,11 +790,12 @@ int sep_fused_dmma3_launch(const double* src, double* dst, const Dims& d, const 
     switch (cfg) {
         // measurement variants (tools/time_fused.py with H3_DMMA_CFG=k)
         case 6: return launch_dm3<Dm3Cfg<7, 16, 3, true>>(src, dst, d, ops, off, st, first_bad, guard);  // cp.async loads
-        case 8: return launch_dm3<Dm3Cfg<7, 16, 4, true, 1, 0, true>>(src, dst, d, ops, off, st, first_bad, guard);
         case 9: return launch_dm3v2<Dm3v2Cfg<7, 3>>(src, dst, d, ops, off, st, first_bad, guard);  // bulk stores
         case 11: return launch_dm3<Dm3Cfg<7, 16, 3, true, 1, 1, true>>(src, dst, d, ops, off, st, first_bad, guard);
         case 14: return launch_dm3<Dm3Cfg<7, 16, 3, true, 1, 4, true>>(src, dst, d, ops, off, st, first_bad, guard);
         case 15: return launch_dm3<Dm3Cfg<7, 16, 3, true, 1, 5, true>>(src, dst, d, ops, off, st, first_bad, guard);
+        case 20: return launch_dm3<Dm3Cfg<7, 16, 3, true, 1, 0, true, true>>(src, dst, d, ops, off, st, first_bad, guard);
+        case 22: return launch_dm3<Dm3Cfg<3, 8, 3, true, 2, 0, true>>(src, dst, d, ops, off, st, first_bad, guard);
         default: return launch_dm3<Dm3Cfg<7, 16, 3, true, 1, 0, true>>(src, dst, d, ops, off, st, first_bad, guard);
     }
 }
