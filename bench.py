@@ -303,7 +303,7 @@ def main():
                      "frac": (achieved / peak_gbs) if achieved else None, "traffic": traffic,
                      "traffic_unit": "DRAM bytes per launch (ncu dram__bytes_read+write)",
                      "traffic_source": traffic_src,
-                     "kernel": ("sep_fused_dmma3_kernel (DMMA m8n8k4, 8x7 tile, 16 warps, TMA row loads)" if order_n == 3
+                     "kernel": ("sep_fused_dmma3_kernel (DMMA m8n8k4, 8x7 tile, 16 warps, TMA row loads, x3/x1 plane pipelining)" if order_n == 3
                                 else ("sep_fused_dmma_cp_kernel<5> (DMMA cell-pair)" if order_n == 5
                                       else f"sep_fused_kernel<{order_n}>")) if args.mode == "fused" else "recon+evolve",
                      "algorithmic_bytes_per_launch": alg_bytes, "mean_launch_ms": launch_ms,

@@ -85,8 +85,11 @@ __device__ __forceinline__ void fence_proxy_async_smem() {
 // ABL (measurement-only ablations, results are garbage): bit 0 skips the global stores,
 // bit 1 the input copies, bit 2 replaces every DMMA by a register update.
 template <int TY_, int WARPS_, int STAGES_, bool VALIAS_, int MINB_ = 1, int ABL_ = 0, bool TMA_ = false,
-          bool LEAN_ = false>
+          bool LEAN_ = false, int PIPE_ = 0>
 struct Dm3Cfg {
+    // PIPE 1: x3 of plane p-1 shares a barrier interval with x1 of plane p (2 barriers/plane);
+    // PIPE 2: x3(p-2), x2(p-1) and x1(p) share one interval (1 barrier/plane, W and V doubled)
+    static constexpr int PIPE = PIPE_;
     static constexpr int ABL = ABL_;
     static constexpr bool TMA = TMA_;
     // LEAN: x3 stores each chain's finished lanes with predicated half-warp stores at 32-bit
@@ -108,7 +111,8 @@ struct Dm3Cfg {
     static constexpr size_t U_D = (size_t)NCOL * UNS;
     static constexpr size_t W_D = (size_t)NY * TX * WCS;
     static constexpr size_t V_D = (size_t)TY * TX * VCS;
-    static constexpr size_t SMEM_DATA = (STAGES * U_D + W_D + (VALIAS ? 0 : V_D)) * sizeof(double);
+    static constexpr size_t SMEM_DATA =
+        (STAGES * U_D + (PIPE == 2 ? 2 : 1) * W_D + (VALIAS ? 0 : (PIPE == 2 ? 2 : 1) * V_D)) * sizeof(double);
     static constexpr size_t SMEM = SMEM_DATA + (TMA ? STAGES * sizeof(uint64_t) : 0);
     static_assert(!TMA || NY <= WARPS, "one loader warp per tile row");
     static_assert(T3 % WARPS == 0, "x3 chains must divide evenly among warps");
@@ -129,7 +133,7 @@ sep_fused_dmma3_kernel(const double* __restrict__ src, double* __restrict__ dst,
     extern __shared__ __align__(16) unsigned char smem_raw[];
     double* U = reinterpret_cast<double*>(smem_raw);
     double* W = U + STAGES * C::U_D;
-    double* Vfix = W + C::W_D;
+    double* Vfix = W + (C::PIPE == 2 ? 2 : 1) * C::W_D;  // PIPE 2: W[2], then V[2]
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int q = lane & 3, g = lane >> 2, par = q >> 1;  // fragment coordinates
@@ -254,19 +258,9 @@ sep_fused_dmma3_kernel(const double* __restrict__ src, double* __restrict__ dst,
 #pragma unroll
     for (int k = 0; k < K3; ++k) acc[k][0] = acc[k][1] = 0.0;
 
-    for (int pl = 0; pl < P; ++pl) {
-        if constexpr (C::TMA) {
-            __syncthreads();
-            issue();  // the stage it fills was last read before the barrier above
-            if (!(C::ABL & 2)) mbar_wait(&bars[pl % STAGES], (unsigned)((pl / STAGES) & 1));
-        } else {
-            cp_async_wait<STAGES - 2>();
-            __syncthreads();
-            issue();  // the stage it fills was last read before the barrier above
-        }
-        const double* Ub = U + (pl % STAGES) * C::U_D;
-        double* V = C::VALIAS ? U + (pl % STAGES) * C::U_D : Vfix;
-
+    // three passes per node plane; PIPE overlaps x3 of plane p-1 with x1 of plane p in one
+    // barrier interval (2 barriers per plane instead of 3; needs the non-aliased V buffer)
+    auto x1_pass = [&](const double* Ub, double* W) {
         // ---- x1: (row ly, half h) chains walk the nodes of their row ------------------------
         // Completed cells alternate between the lane halves; an even cell's values are
         // held one node longer so both halves store together (full-warp STS).
@@ -310,8 +304,8 @@ sep_fused_dmma3_kernel(const double* __restrict__ src, double* __restrict__ dst,
                 }
             }
         }
-        __syncthreads();
-
+    };
+    auto x2_pass = [&](const double* W, double* V) {
         // ---- x2: (column ix, half h) chains walk the rows of their column -----------------
         {
             const double* wa[K2];
@@ -361,13 +355,13 @@ sep_fused_dmma3_kernel(const double* __restrict__ src, double* __restrict__ dst,
                 }
             }
         }
-        __syncthreads();
-
+    };
+    auto x3_pass = [&](const double* V, const int pp) {
         // ---- x3: each warp advances its chains by one plane ---------------------------------
         // Chain k runs with column phase (k & 1), so chains 2j and 2j+1 complete in opposite
         // lane halves and share one full-warp store.
         {
-            const int64_t plane_off = (int64_t)(pl - 1) * plane_elems;
+            const int64_t plane_off = (int64_t)(pp - 1) * plane_elems;
             double v0[K3], v1[K3];
 #pragma unroll
             for (int k = 0; k < K3; ++k) {
@@ -375,21 +369,21 @@ sep_fused_dmma3_kernel(const double* __restrict__ src, double* __restrict__ dst,
                 const int cell = t >> 1, h = t & 1;
                 const int L = 8 * h + g;  // line (m2, m1) = (L >> 2, L & 3)
                 const double a = V[cell * VCS + (L >> 2) * VRS + (L & 3) * 4 + q];
-                const int ph = (pl + k) & 1;
+                const int ph = (pp + k) & 1;
                 dmma_abl<C::ABL>(acc[k][0], acc[k][1], a, ph ? bop[2][1] : bop[2][0]);
-                const bool done = par == ((pl + k + 1) & 1);
+                const bool done = par == ((pp + k + 1) & 1);
                 v0[k] = acc[k][0];
                 v1[k] = acc[k][1];
                 acc[k][0] = done ? 0.0 : acc[k][0];
                 acc[k][1] = done ? 0.0 : acc[k][1];
             }
             if constexpr (C::LEAN) {
-                if (pl > 0) {
-                    double* oplane = dst + (zc0 + pl - 1) * plane_elems;
+                if (pp > 0) {
+                    double* oplane = dst + (zc0 + pp - 1) * plane_elems;
                     unsigned screen = 0x7ff00000u;
 #pragma unroll
                     for (int k = 0; k < K3; ++k) {
-                        const bool done = par == ((pl + k + 1) & 1);
+                        const bool done = par == ((pp + k + 1) & 1);
                         if (done && ooff[k] >= 0) {
                             if (!(C::ABL & 1)) {
                                 __stcs(oplane + ooff[k], v0[k]);
@@ -402,17 +396,17 @@ sep_fused_dmma3_kernel(const double* __restrict__ src, double* __restrict__ dst,
                     if (screen == 0u) {  // rare: some lane holds Inf/NaN (finished or partial)
 #pragma unroll
                         for (int k = 0; k < K3; ++k) {
-                            const bool done = par == ((pl + k + 1) & 1);
+                            const bool done = par == ((pp + k + 1) & 1);
                             if (done && ooff[k] >= 0 && (!isfinite(v0[k]) || !isfinite(v1[k])))
-                                flag_bad(first_bad, (zc0 + pl - 1) * M2 * (int64_t)M1 + ooff[k] / n3);
+                                flag_bad(first_bad, (zc0 + pp - 1) * M2 * (int64_t)M1 + ooff[k] / n3);
                         }
                     }
                 }
-            } else if (pl > 0) {
+            } else if (pp > 0) {
 #pragma unroll
                 for (int k = 0; k < K3; k += 2) {
-                    // lanes with par == ((pl + k + 1) & 1) hold chain k, the others chain k+1
-                    const bool mine = par == ((pl + k + 1) & 1);
+                    // lanes with par == ((pp + k + 1) & 1) hold chain k, the others chain k+1
+                    const bool mine = par == ((pp + k + 1) & 1);
                     const bool pair = k + 1 < K3;
                     if (!pair && !mine) continue;  // odd chain count: lone last chain
                     const int k2 = pair ? k + 1 : k;
@@ -430,6 +424,49 @@ sep_fused_dmma3_kernel(const double* __restrict__ src, double* __restrict__ dst,
                     }
                 }
             }
+        }
+    };
+    auto top = [&](int pl) {
+        if constexpr (C::TMA) {
+            __syncthreads();
+            issue();  // the stage it fills was last read before the barrier above
+            if (!(C::ABL & 2)) mbar_wait(&bars[pl % STAGES], (unsigned)((pl / STAGES) & 1));
+        } else {
+            cp_async_wait<STAGES - 2>();
+            __syncthreads();
+            issue();  // the stage it fills was last read before the barrier above
+        }
+    };
+    if constexpr (C::PIPE == 2) {
+        static_assert(!C::VALIAS, "PIPE keeps V(p-1) while stage p is refilled");
+        double* Wb[2] = {W, W + C::W_D};
+        double* Vb[2] = {Vfix, Vfix + C::V_D};
+        for (int pl = 0; pl <= P + 1; ++pl) {
+            if (pl < P) top(pl);
+            else __syncthreads();
+            if (pl >= 2) x3_pass(Vb[pl & 1], pl - 2);
+            if (pl >= 1 && pl <= P) x2_pass(Wb[(pl - 1) & 1], Vb[(pl - 1) & 1]);
+            if (pl < P) x1_pass(U + (pl % STAGES) * C::U_D, Wb[pl & 1]);
+        }
+    } else if constexpr (C::PIPE == 1) {
+        static_assert(!C::VALIAS, "PIPE keeps V(p-1) while stage p is refilled");
+        for (int pl = 0; pl <= P; ++pl) {
+            if (pl < P) top(pl);
+            else __syncthreads();
+            if (pl >= 1) x3_pass(Vfix, pl - 1);
+            if (pl < P) x1_pass(U + (pl % STAGES) * C::U_D, W);
+            __syncthreads();
+            if (pl < P) x2_pass(W, Vfix);
+        }
+    } else {
+        for (int pl = 0; pl < P; ++pl) {
+            top(pl);
+            double* V = C::VALIAS ? U + (pl % STAGES) * C::U_D : Vfix;
+            x1_pass(U + (pl % STAGES) * C::U_D, W);
+            __syncthreads();
+            x2_pass(W, V);
+            __syncthreads();
+            x3_pass(V, pl);
         }
     }
     cp_async_wait<0>();
@@ -796,7 +833,12 @@ int sep_fused_dmma3_launch(const double* src, double* dst, const Dims& d, const 
         case 15: return launch_dm3<Dm3Cfg<7, 16, 3, true, 1, 5, true>>(src, dst, d, ops, off, st, first_bad, guard);
         case 20: return launch_dm3<Dm3Cfg<7, 16, 3, true, 1, 0, true, true>>(src, dst, d, ops, off, st, first_bad, guard);
         case 22: return launch_dm3<Dm3Cfg<3, 8, 3, true, 2, 0, true>>(src, dst, d, ops, off, st, first_bad, guard);
-        default: return launch_dm3<Dm3Cfg<7, 16, 3, true, 1, 0, true>>(src, dst, d, ops, off, st, first_bad, guard);
+        case 25: return launch_dm3<Dm3Cfg<7, 16, 3, false, 1, 0, true, false, 1>>(src, dst, d, ops, off, st, first_bad, guard);
+        case 27: return launch_dm3<Dm3Cfg<6, 16, 3, false, 1, 0, true, true, 2>>(src, dst, d, ops, off, st, first_bad, guard);
+        case 28: return launch_dm3<Dm3Cfg<6, 16, 3, false, 1, 0, true, true, 1>>(src, dst, d, ops, off, st, first_bad, guard);
+        case 16: return launch_dm3<Dm3Cfg<7, 16, 3, true, 1, 0, true>>(src, dst, d, ops, off, st, first_bad, guard);
+        // default: TMA row loads, x3(p-1) pipelined with x1(p) (2 barriers per plane), lean x3 stores
+        default: return launch_dm3<Dm3Cfg<7, 16, 3, false, 1, 0, true, true, 1>>(src, dst, d, ops, off, st, first_bad, guard);
     }
 }
 
