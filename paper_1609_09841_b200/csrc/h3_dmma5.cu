@@ -190,13 +190,40 @@ sep_fused_dmma_cp_kernel(const double* __restrict__ src, double* __restrict__ ds
         o3[it] = (l < L2 && qout && cx < M1 && cy < M2) ? (cy * M1 + cx) * n3 + (2 * q) * n2 + r : -1;
     }
 
-    for (int pl = 0; pl < P; ++pl) {
-        __syncthreads();
-        issue();  // refills the stage read in iteration pl - 1
-        mbar_wait(&bars[pl % STAGES], (unsigned)((pl / STAGES) & 1));
-        const double* Ub = U + (pl % STAGES) * C::U_D;
-        double* Vc = V + (pl & 1) * C::V_D;
-
+    // x3 of cell plane p-2 shares a barrier interval with x1 of node plane p (2 barriers per plane)
+    for (int pl = 0; pl <= P; ++pl) {
+        if (pl < P) {
+            __syncthreads();
+            issue();  // refills the stage read in iteration pl - 1
+            mbar_wait(&bars[pl % STAGES], (unsigned)((pl / STAGES) & 1));
+        } else {
+            __syncthreads();
+        }
+        // ---- x3: line cell n^2 + (m2 n + m1), V planes p-1 and p -> dst (cell plane p-1) --------
+        if (pl >= 2) {
+            const int cp = pl - 2;  // cell plane (node planes cp, cp + 1)
+            const double* vk[KS];
+#pragma unroll
+            for (int ks = 0; ks < KS; ++ks) vk[ks] = V + ((cp + ka[ks]) & 1) * C::V_D + k3[ks];
+            double* oplane = dst + (zc0 + cp) * plane_elems;
+            double d[I3][2];
+#pragma unroll
+            for (int it = 0; it < I3; ++it) {
+                d[it][0] = d[it][1] = 0.0;
+#pragma unroll
+                for (int ks = 0; ks < KS; ++ks) dmma(d[it][0], d[it][1], vk[ks][r3[it]], bop[2][ks]);
+            }
+#pragma unroll
+            for (int it = 0; it < I3; ++it)
+                if (o3[it] >= 0) {
+                    __stcs(oplane + o3[it], d[it][0]);
+                    __stcs(oplane + o3[it] + n2, d[it][1]);
+                    if (!isfinite(d[it][0]) || !isfinite(d[it][1]))
+                        flag_bad(first_bad, (zc0 + cp) * M2 * (int64_t)M1 + o3[it] / n3);
+                }
+        }
+        if (pl < P) {
+            const double* Ub = U + (pl % STAGES) * C::U_D;
         // ---- x1: line (ly TX + cx) n^2 + jj:  U(p) -> W ------------------------------------------
         {
             double d[I1][2];
@@ -213,8 +240,10 @@ sep_fused_dmma_cp_kernel(const double* __restrict__ src, double* __restrict__ ds
                     W[w1[it] + WM] = d[it][1];
                 }
         }
+        }
         __syncthreads();
-
+        if (pl < P) {
+            double* Vc = V + (pl & 1) * C::V_D;
         // ---- x2: line cell n^2 + j3 n + m1:  W -> V[p & 1] ---------------------------------------
         {
             double d[I2][2];
@@ -231,29 +260,6 @@ sep_fused_dmma_cp_kernel(const double* __restrict__ src, double* __restrict__ ds
                     Vc[w2[it] + n] = d[it][1];
                 }
         }
-        __syncthreads();
-
-        // ---- x3: line cell n^2 + (m2 n + m1), V planes p-1 and p -> dst (cell plane p-1) --------
-        if (pl > 0) {
-            const double* vk[KS];
-#pragma unroll
-            for (int ks = 0; ks < KS; ++ks) vk[ks] = V + ((pl - 1 + ka[ks]) & 1) * C::V_D + k3[ks];
-            double* oplane = dst + (zc0 + pl - 1) * plane_elems;
-            double d[I3][2];
-#pragma unroll
-            for (int it = 0; it < I3; ++it) {
-                d[it][0] = d[it][1] = 0.0;
-#pragma unroll
-                for (int ks = 0; ks < KS; ++ks) dmma(d[it][0], d[it][1], vk[ks][r3[it]], bop[2][ks]);
-            }
-#pragma unroll
-            for (int it = 0; it < I3; ++it)
-                if (o3[it] >= 0) {
-                    __stcs(oplane + o3[it], d[it][0]);
-                    __stcs(oplane + o3[it] + n2, d[it][1]);
-                    if (!isfinite(d[it][0]) || !isfinite(d[it][1]))
-                        flag_bad(first_bad, (zc0 + pl - 1) * M2 * (int64_t)M1 + o3[it] / n3);
-                }
         }
     }
 }
@@ -430,13 +436,41 @@ recon_dmma_cp_kernel(const double* __restrict__ src, double* __restrict__ coeff,
         o3[it] = (l < L3 && cx < M1 && cy < M2) ? (cy * M1 + cx) * S3 + (2 * q) * S2 + r : -1;  // + 8 cb S2
     }
 
-    for (int pl = 0; pl < P; ++pl) {
-        __syncthreads();
-        issue();
-        mbar_wait(&bars[pl % STAGES], (unsigned)((pl / STAGES) & 1));
-        const double* Ub = U + (pl % STAGES) * C::U_D;
-        double* Vc = V + (pl & 1) * C::V_D;
-
+    // x3 of cell plane p-2 shares a barrier interval with x1 of node plane p (2 barriers per plane)
+    for (int pl = 0; pl <= P; ++pl) {
+        if (pl < P) {
+            __syncthreads();
+            issue();  // refills the stage read in iteration pl - 1
+            mbar_wait(&bars[pl % STAGES], (unsigned)((pl / STAGES) & 1));
+        } else {
+            __syncthreads();
+        }
+        // ---- x3: V planes p-1, p -> coeff (cell plane p-1), streaming stores ------------------
+        if (pl >= 2) {
+            const int cp = pl - 2;  // cell plane (node planes cp, cp + 1)
+            const double* vk[KS];
+#pragma unroll
+            for (int ks = 0; ks < KS; ++ks) vk[ks] = V + ((cp + ka[ks]) & 1) * C::V_D + k3[ks];
+            double* oplane = coeff + (zc0 - d.z_begin + cp) * cplane;
+#pragma unroll
+            for (int it = 0; it < I3; ++it) {
+                double a[KS];
+#pragma unroll
+                for (int ks = 0; ks < KS; ++ks) a[ks] = vk[ks][r3[it]];
+#pragma unroll
+                for (int cb = 0; cb < CB; ++cb) {
+                    double d0 = 0.0, d1 = 0.0;
+#pragma unroll
+                    for (int ks = 0; ks < KS; ++ks) dmma(d0, d1, a[ks], bop[ks][cb]);
+                    if (o3[it] >= 0 && (cb < CB - 1 || cout1)) {
+                        __stcs(oplane + o3[it] + 8 * cb * S2, d0);
+                        __stcs(oplane + o3[it] + (8 * cb + 1) * S2, d1);
+                    }
+                }
+            }
+        }
+        if (pl < P) {
+            const double* Ub = U + (pl % STAGES) * C::U_D;
         // ---- x1: U(p) -> W[row][cell][i1][j3 j2] ----------------------------------------------
 #pragma unroll
         for (int it = 0; it < I1; ++it) {
@@ -454,8 +488,10 @@ recon_dmma_cp_kernel(const double* __restrict__ src, double* __restrict__ coeff,
                 }
             }
         }
+        }
         __syncthreads();
-
+        if (pl < P) {
+            double* Vc = V + (pl & 1) * C::V_D;
         // ---- x2: W -> V[p & 1][cell][j3][i2 i1] -------------------------------------------------
 #pragma unroll
         for (int it = 0; it < I2; ++it) {
@@ -473,30 +509,6 @@ recon_dmma_cp_kernel(const double* __restrict__ src, double* __restrict__ coeff,
                 }
             }
         }
-        __syncthreads();
-
-        // ---- x3: V planes p-1, p -> coeff (cell plane p-1), streaming stores ------------------
-        if (pl > 0) {
-            const double* vk[KS];
-#pragma unroll
-            for (int ks = 0; ks < KS; ++ks) vk[ks] = V + ((pl - 1 + ka[ks]) & 1) * C::V_D + k3[ks];
-            double* oplane = coeff + (zc0 - d.z_begin + pl - 1) * cplane;
-#pragma unroll
-            for (int it = 0; it < I3; ++it) {
-                double a[KS];
-#pragma unroll
-                for (int ks = 0; ks < KS; ++ks) a[ks] = vk[ks][r3[it]];
-#pragma unroll
-                for (int cb = 0; cb < CB; ++cb) {
-                    double d0 = 0.0, d1 = 0.0;
-#pragma unroll
-                    for (int ks = 0; ks < KS; ++ks) dmma(d0, d1, a[ks], bop[ks][cb]);
-                    if (o3[it] >= 0 && (cb < CB - 1 || cout1)) {
-                        __stcs(oplane + o3[it] + 8 * cb * S2, d0);
-                        __stcs(oplane + o3[it] + (8 * cb + 1) * S2, d1);
-                    }
-                }
-            }
         }
     }
 }
