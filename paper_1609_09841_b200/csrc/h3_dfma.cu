@@ -237,10 +237,7 @@ static int recon_sep_ns(const double* src, double* coeff, const Dims& d, int off
     e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, G::THREADS, G::SMEM);
     if (e != cudaSuccess) return (int)e;
     const int64_t gx = (d.M1 + G::TX - 1) / G::TX, gy = (d.M2 + G::TY - 1) / G::TY;
-    const int64_t want = (int64_t)num_sms() * (per_sm > 0 ? per_sm : 1) * 4;
-    int64_t zsplit = (want + gx * gy - 1) / (gx * gy);
-    int64_t zchunk = (nz + zsplit - 1) / zsplit;
-    if (zchunk < 8) zchunk = nz < 8 ? nz : 8;
+    const int64_t zchunk = choose_zchunk(gx * gy, nz, (int64_t)num_sms() * (per_sm > 0 ? per_sm : 1));
     const int64_t gz = (nz + zchunk - 1) / zchunk;
     kern<<<dim3((unsigned)gx, (unsigned)gy, (unsigned)gz), G::THREADS, G::SMEM, st>>>(
         src, coeff, d, off, (int)zchunk, guard);

@@ -732,10 +732,7 @@ static int launch_dm3v2(const double* src, double* dst, const Dims& d, const Sep
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM);
     if (e != cudaSuccess) return (int)e;
     const int64_t gx = (d.M1 + C::TX - 1) / C::TX, gy = (d.M2 + C::TY - 1) / C::TY;
-    const int64_t want = (int64_t)num_sms() * 4;
-    int64_t zsplit = (want + gx * gy - 1) / (gx * gy);
-    int64_t zchunk = (nz + zsplit - 1) / zsplit;
-    if (zchunk < 8) zchunk = nz < 8 ? nz : 8;
+    const int64_t zchunk = choose_zchunk(gx * gy, nz, num_sms());  // one CTA per SM
     const int64_t gz = (nz + zchunk - 1) / zchunk;
     static const int cy = [] {
         const char* s = getenv("H3_DMMA_CLUSTER_Y");
@@ -773,10 +770,7 @@ static int launch_dm3(const double* src, double* dst, const Dims& d, const SepOp
     e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, C::THREADS, C::SMEM);
     if (e != cudaSuccess) return (int)e;
     const int64_t gx = (d.M1 + C::TX - 1) / C::TX, gy = (d.M2 + C::TY - 1) / C::TY;
-    const int64_t want = (int64_t)num_sms() * (per_sm > 0 ? per_sm : 1) * 4;
-    int64_t zsplit = (want + gx * gy - 1) / (gx * gy);
-    int64_t zchunk = (nz + zsplit - 1) / zsplit;
-    if (zchunk < 8) zchunk = nz < 8 ? nz : 8;
+    const int64_t zchunk = choose_zchunk(gx * gy, nz, (int64_t)num_sms() * (per_sm > 0 ? per_sm : 1));
     const int64_t gz = (nz + zchunk - 1) / zchunk;
     // Thread-block clusters of 2 tiles along x2 (H3_DMMA_CLUSTER_Y, 1 = off): y-adjacent tiles
     // share a node row; co-scheduling them keeps that row in L2 for the second reader
@@ -1049,10 +1043,7 @@ int recon_dmma3_launch(const double* src, double* coeff, const Dims& d, const do
     cudaError_t e = cudaFuncSetAttribute(recon_dmma3_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM);
     if (e != cudaSuccess) return (int)e;
     const int64_t gx = (d.M1 + TX - 1) / TX, gy = (d.M2 + TY - 1) / TY;
-    const int64_t want = (int64_t)num_sms() * 4;
-    int64_t zsplit = (want + gx * gy - 1) / (gx * gy);
-    int64_t zchunk = (nz + zsplit - 1) / zsplit;
-    if (zchunk < 8) zchunk = nz < 8 ? nz : 8;
+    const int64_t zchunk = choose_zchunk(gx * gy, nz, num_sms());  // one CTA per SM
     const int64_t gz = (nz + zchunk - 1) / zchunk;
     recon_dmma3_kernel<<<dim3((unsigned)gx, (unsigned)gy, (unsigned)gz), THREADS, SMEM, st>>>(
         src, coeff, d, off, (int)zchunk, hp, guard);

@@ -281,10 +281,7 @@ static int launch_cp(const double* src, double* dst, const Dims& d, const double
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM);
     if (e != cudaSuccess) return (int)e;
     const int64_t gx = (d.M1 + C::TX - 1) / C::TX, gy = (d.M2 + C::TY - 1) / C::TY;
-    const int64_t want = (int64_t)num_sms() * 4;
-    int64_t zsplit = (want + gx * gy - 1) / (gx * gy);
-    int64_t zchunk = (nz + zsplit - 1) / zsplit;
-    if (zchunk < 8) zchunk = nz < 8 ? nz : 8;
+    const int64_t zchunk = choose_zchunk(gx * gy, nz, num_sms());  // one CTA per SM
     const int64_t gz = (nz + zchunk - 1) / zchunk;
     kern<<<dim3((unsigned)gx, (unsigned)gy, (unsigned)gz), C::THREADS, C::SMEM, st>>>(src, dst, d, off, (int)zchunk,
                                                                                    ops, first_bad, guard);
@@ -528,10 +525,7 @@ int recon_dmma5_launch(const double* src, double* coeff, const Dims& d, const do
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM);
     if (e != cudaSuccess) return (int)e;
     const int64_t gx = (d.M1 + C::TX - 1) / C::TX, gy = (d.M2 + C::TY - 1) / C::TY;
-    const int64_t want = (int64_t)num_sms() * 4;
-    int64_t zsplit = (want + gx * gy - 1) / (gx * gy);
-    int64_t zchunk = (nz + zsplit - 1) / zsplit;
-    if (zchunk < 8) zchunk = nz < 8 ? nz : 8;
+    const int64_t zchunk = choose_zchunk(gx * gy, nz, num_sms());  // one CTA per SM
     const int64_t gz = (nz + zchunk - 1) / zchunk;
     kern<<<dim3((unsigned)gx, (unsigned)gy, (unsigned)gz), C::THREADS, C::SMEM, st>>>(src, coeff, d, off, (int)zchunk,
                                                                                    hp, guard);

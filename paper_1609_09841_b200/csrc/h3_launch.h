@@ -80,4 +80,28 @@ int check_finite_launch(const double* field, int64_t M1, int64_t M2, int64_t M3,
 
 int num_sms();
 
+// z-chunk length for a tile march over nz cell planes with `tiles` x1-x2 tiles and `slots`
+// resident CTAs: minimises waves x (planes per CTA + halo plane + ~2 planes of pipeline fill),
+// waves = ceil(tiles * chunks / slots), over chunk lengths >= min_chunk.  (At 512^3 m=3 this is
+// one chunk per tile -- 4736 tiles = 32 full waves; at 128^3 it avoids a 10 %-full last wave.)
+inline int64_t choose_zchunk(int64_t tiles, int64_t nz, int64_t slots, int64_t min_chunk = 8) {
+    if (nz <= min_chunk) return nz > 0 ? nz : 1;
+    if (slots < 1) slots = 1;
+    int64_t best = nz;
+    double best_cost = 1e300;
+    for (int64_t zs = 1;; ++zs) {
+        const int64_t zc = (nz + zs - 1) / zs;
+        if (zc < min_chunk) break;
+        const int64_t chunks = (nz + zc - 1) / zc;
+        const int64_t waves = (tiles * chunks + slots - 1) / slots;
+        const double cost = (double)waves * (double)(zc + 3);
+        if (cost < best_cost * (1.0 - 1e-9)) {
+            best_cost = cost;
+            best = zc;
+        }
+        if (zc == min_chunk) break;
+    }
+    return best;
+}
+
 }  // namespace h3

@@ -260,10 +260,7 @@ static int sep_fused_n(const double* src, double* dst, const Dims& d, const doub
     if (e != cudaSuccess) return (int)e;
     const int64_t gx = (d.M1 + G::TX - 1) / G::TX, gy = (d.M2 + G::TY - 1) / G::TY;
     // enough CTAs for ~4 waves; split the z march only when the x-y tiling is too coarse
-    const int64_t want = (int64_t)num_sms() * (per_sm > 0 ? per_sm : 1) * 4;
-    int64_t zsplit = (want + gx * gy - 1) / (gx * gy);
-    int64_t zchunk = (nz + zsplit - 1) / zsplit;
-    if (zchunk < 8) zchunk = nz < 8 ? nz : 8;
+    const int64_t zchunk = choose_zchunk(gx * gy, nz, (int64_t)num_sms() * (per_sm > 0 ? per_sm : 1));
     const int64_t gz = (nz + zchunk - 1) / zchunk;
     dim3 grid((unsigned)gx, (unsigned)gy, (unsigned)gz);
     kern<<<grid, G::THREADS, G::SMEM, st>>>(src, dst, d, off, (int)zchunk, ops, first_bad, guard);
