@@ -1,0 +1,258 @@
+"""Run orchestration on the B200: the reference runner's stepping loop, with the GPU kept busy.
+
+Mirror of `execute_run` / `execute_converge` (reference pkg/src/hermite3d/runner.py:135-230)
+for library callers: same step planning (`_plan_steps`, runner.py:65-76), the same artifacts
+(snapshot.bin/json, errors.csv, perf.json/perf.csv) and the same summary keys.  The reference's
+pydantic RunConfig / CLI / REST layers are out of scope; `RunConfig` here is a
+plain dataclass with the same fields and validation messages, and `build_ic` understands the
+reference's IC term dictionaries (`plane_wave`, `random_modes`, `separable` with
+`fourier` / `constant` / `monomial` factors, config.py:30-70, 133-153).
+
+B200 difference: the reference evaluates the error norms on the host after every step, which
+would force a device synchronisation per step.  Here every half step and every per-step error
+reduction is queued on the stream (h3_error_norms writes into a device array) and the flags and
+norms are read back once at the end; an instability still raises InstabilityError naming the
+reference's step and node (later half steps are skipped on the device by the guard flags).
+"""
+
+from __future__ import annotations
+
+import csv
+import json
+import math
+from dataclasses import dataclass, field as dc_field, replace
+from pathlib import Path
+
+import numpy as np
+import torch
+
+from . import perf
+from .field import DofField, GridSpec, write_snapshot
+from .pipeline import AllocationStats, InstabilityError, OperatorSet, StepConfig, _new_flags, _node_of, half_step, \
+    select_dt
+from .problems import Constant, FourierMode, Monomial, SeparableIC, error_norms_async, exact_solution, init_field, \
+    plane_wave
+
+__all__ = ["RunConfig", "ConfigError", "build_ic", "execute_run", "execute_converge"]
+
+
+class ConfigError(ValueError):
+    """Invalid run configuration (reference config.ConfigError)."""
+
+
+@dataclass(frozen=True)
+class RunConfig:
+    """Everything one run needs (reference config.py:73-122; order cap lifted to 5)."""
+
+    order_n: int
+    cells: tuple
+    domain: tuple = (1.0, 1.0, 1.0)
+    cfl: float = 0.9
+    stages_q: int | None = None
+    steps: int | None = None
+    final_time: float | None = None
+    mode: str = "fused"
+    tile_x1: int | None = None
+    precision: str = "double"
+    variant: str = "auto"
+    ic: tuple = dc_field(default_factory=lambda: ({"kind": "plane_wave"},))
+    seed: int = 0
+    out_dir: str = "out"
+
+    def __post_init__(self):
+        cells = (self.cells,) * 3 if isinstance(self.cells, int) else tuple(self.cells)
+        object.__setattr__(self, "cells", cells)
+        object.__setattr__(self, "domain", tuple(float(x) for x in self.domain))
+        if not 0 <= self.order_n <= 5:
+            raise ConfigError("order_n: must be in [0, 5]")
+        if len(cells) != 3 or any(int(m) != m or m < 1 for m in cells):
+            raise ConfigError("cells: all cell counts must be >= 1")
+        if len(self.domain) != 3 or any(not (l > 0) for l in self.domain):
+            raise ConfigError("domain: all domain lengths must be positive")
+        if not 0 < self.cfl <= 1:
+            raise ConfigError("cfl: must be in (0, 1]")
+        if (self.steps is None) == (self.final_time is None):
+            raise ConfigError("steps/final_time: exactly one of steps or final_time must be set")
+        if self.steps is not None and self.steps < 1:
+            raise ConfigError("steps: must be >= 1")
+        if self.final_time is not None and not self.final_time > 0:
+            raise ConfigError("final_time: must be > 0")
+        if self.mode not in ("fused", "two_pass"):
+            raise ConfigError("mode: must be 'fused' or 'two_pass'")
+        if self.precision not in ("double", "single"):
+            raise ConfigError("precision: must be 'double' or 'single'")
+        if not self.ic:
+            raise ConfigError("ic: at least one term is required")
+
+    def stages(self) -> int:
+        return self.stages_q if self.stages_q is not None else 3 * (2 * self.order_n + 1)
+
+    def step_config(self) -> StepConfig:
+        return StepConfig(mode=self.mode, tile_x1=self.tile_x1, cfl=self.cfl, stages_q=self.stages(),
+                          precision=self.precision, variant=self.variant)
+
+
+def _factor(f: dict):
+    kind = f.get("kind", "fourier")
+    if kind == "fourier":
+        return FourierMode(amplitude=float(f.get("amplitude", 1.0)), wavenumber=int(f.get("wavenumber", 1)),
+                           phase=float(f.get("phase", 0.0)))
+    if kind == "constant":
+        return Constant(float(f.get("value", 1.0)))
+    if kind == "monomial":
+        return Monomial(int(f.get("degree", 1)))
+    raise ConfigError(f"ic: unknown factor kind {kind!r}")
+
+
+def build_ic(cfg: RunConfig) -> SeparableIC:
+    """Expand the config's IC terms into a separable IC (reference config.py:133-153)."""
+    if isinstance(cfg.ic, SeparableIC):
+        return cfg.ic
+    terms = []
+    rng = np.random.default_rng(cfg.seed)
+    for term in cfg.ic:
+        kind = term.get("kind", "plane_wave")
+        if kind == "separable":
+            terms.append(tuple(_factor(f) for f in term["factors"]))
+        elif kind == "plane_wave":
+            terms.extend(plane_wave(int(term.get("wavenumber", 1)), float(term.get("amplitude", 1.0)),
+                                    float(term.get("phase", 0.0))).terms)
+        elif kind == "random_modes":
+            for _ in range(int(term.get("terms", 4))):
+                terms.append(tuple(FourierMode(amplitude=float(rng.uniform(-1.0, 1.0)),
+                                               wavenumber=int(rng.integers(1, int(term.get("max_wavenumber", 2)) + 1)),
+                                               phase=float(rng.uniform(0.0, 2 * np.pi)))
+                                   for _ in range(3)))
+        else:
+            raise ConfigError(f"ic: unknown term kind {kind!r}")
+    return SeparableIC(terms=tuple(terms))
+
+
+def _plan_steps(cfg: RunConfig, grid: GridSpec, step_cfg: StepConfig) -> tuple[int, float]:
+    """Number of full steps and the effective dt (reference runner.py:65-76)."""
+    dt_max = select_dt(grid, step_cfg)
+    if cfg.steps is not None:
+        return cfg.steps, dt_max
+    n = max(1, math.ceil(cfg.final_time / dt_max - 1e-12))
+    return n, cfg.final_time / n
+
+
+def _float_cell(x) -> str:
+    return repr(float(x)) if isinstance(x, (float, np.floating)) else str(x)
+
+
+def _write_csv(path: Path, header, rows) -> None:
+    path.parent.mkdir(parents=True, exist_ok=True)
+    with open(path, "w", newline="") as fh:
+        w = csv.writer(fh)
+        w.writerow(header)
+        for row in rows:
+            w.writerow([_float_cell(x) for x in row])
+
+
+def execute_run(cfg: RunConfig, write_artifacts: bool = True) -> dict:
+    """Full time-stepping run; returns the reference's summary dict (+ artifact paths).
+
+    Raises InstabilityError (with the failing step and node) if the field goes non-finite.
+    """
+    step_cfg = cfg.step_config()
+    grid = GridSpec(cfg.cells, cfg.domain, "primary")
+    ops = OperatorSet.for_grid(grid, cfg.order_n)
+    ic = build_ic(cfg)
+    state = init_field(ic, grid, cfg.order_n, precision=cfg.precision)
+    scratch = DofField.zeros(grid.with_parity("dual"), cfg.order_n, precision=cfg.precision)
+    n_steps, dt = _plan_steps(cfg, grid, step_cfg)
+    track = ic.smoothness_class == "analytic" and cfg.precision == "double"
+    stats = AllocationStats()
+    dev = state.device
+    norms = torch.zeros((n_steps + 1, 2), dtype=torch.float64, device=dev)
+    flags = _new_flags(2 * n_steps, dev)
+    stream = torch.cuda.current_stream(dev)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    if track:
+        error_norms_async(state, exact_solution(ic, 0.0, grid.domain_lengths), norms[0])
+    e0.record(stream)
+    prev = None
+    for k in range(n_steps):
+        f0, f1 = flags[2 * k:2 * k + 1], flags[2 * k + 1:2 * k + 2]
+        half_step(state, scratch, step_cfg, ops, stats=stats, dt=dt, step_index=k + 1, _flag=f0, _guard=prev,
+                  _check=False)
+        half_step(scratch, state, step_cfg, ops, stats=stats, dt=dt, step_index=k + 1, _flag=f1, _guard=f0,
+                  _check=False)
+        prev = f1
+        if track:
+            error_norms_async(state, exact_solution(ic, (k + 1) * dt, grid.domain_lengths), norms[k + 1])
+    e1.record(stream)
+    host_flags = flags.cpu().numpy()  # one synchronisation for the whole run
+    for i, bad in enumerate(host_flags):
+        if int(bad) != -1:
+            raise InstabilityError(node=_node_of(int(bad), (scratch.grid, state.grid)[i % 2]), step=i // 2 + 1)
+    wall = e0.elapsed_time(e1) / 1e3
+    t = n_steps * dt
+    h1, h2, h3 = grid.spacings
+    error_rows = []
+    if track:
+        for k, (linf, sumsq) in enumerate(norms.cpu().tolist()):
+            error_rows.append([k, k * dt, linf, math.sqrt(h1 * h2 * h3 * sumsq)])
+    result = {"status": "ok", "steps": n_steps, "dt": dt, "final_time": t, "mode": cfg.mode,
+              "order_n": cfg.order_n, "seconds": wall, "peak_aux_bytes": stats.peak_aux_bytes, "artifacts": {}}
+    if track:
+        result["l_inf"] = error_rows[-1][2]
+        result["l2"] = error_rows[-1][3]
+    if write_artifacts:
+        out_dir = Path(cfg.out_dir)
+        out_dir.mkdir(parents=True, exist_ok=True)
+        bin_path, json_path = write_snapshot(state, out_dir / "snapshot", time=t)
+        result["artifacts"]["snapshot_bin"] = str(bin_path)
+        result["artifacts"]["snapshot_json"] = str(json_path)
+        if track:
+            errors_path = out_dir / "errors.csv"
+            _write_csv(errors_path, ["step", "time", "l_inf", "l2"], error_rows)
+            result["artifacts"]["errors_csv"] = str(errors_path)
+        peaks = perf.DevicePeaks.b200()
+        kernels = ["monolithic"] if cfg.mode == "fused" else ["reconstruction", "evolution"]
+        rows, tf, tb = [], 0, 0
+        for kern in kernels:
+            f1_, b1_ = perf.model_counts(kern, cfg.order_n, grid, step_cfg)
+            f_, b_ = f1_ * 2 * n_steps, b1_ * 2 * n_steps
+            tf, tb = tf + f_, tb + b_
+            tile = perf.resolve_tile_x1(kern, cfg.order_n, grid.cells_per_axis[0], cfg.tile_x1)
+            rows.append(perf._profile(kern, cfg.order_n, cfg.mode, tile, f_, b_, max(wall / len(kernels), 1e-12),
+                                      peaks, perf.algorithmic_bytes(kern, cfg.order_n, grid) * 2 * n_steps))
+        rows.append(perf._profile("solution", cfg.order_n, cfg.mode, rows[0].tile_x1, tf, tb, max(wall, 1e-12),
+                                  peaks))
+        report = perf.report_dict(rows, peaks)
+        (out_dir / "perf.json").write_text(json.dumps(report, sort_keys=True, indent=2) + "\n")
+        _write_csv(out_dir / "perf.csv", perf.REPORT_COLUMNS,
+                   [[run[c] for c in perf.REPORT_COLUMNS] for run in report["runs"]])
+        result["artifacts"]["perf_json"] = str(out_dir / "perf.json")
+        result["artifacts"]["perf_csv"] = str(out_dir / "perf.csv")
+    return result
+
+
+def execute_converge(cfg: RunConfig, levels: list[int]) -> dict:
+    """Refinement study over cubic grids; observed orders between levels (runner.py:198-236)."""
+    if len(levels) < 2:
+        raise ConfigError("levels: need at least two refinement levels")
+    if cfg.final_time is None:
+        raise ConfigError("final_time: converge requires final_time (not steps)")
+    header = ["cells", "h", "l_inf", "l2", "order_linf", "order_l2"]
+    rows, prev = [], None
+    for m in levels:
+        summary = execute_run(replace(cfg, cells=(m, m, m), steps=None), write_artifacts=False)
+        if "l_inf" not in summary:
+            raise ConfigError("ic: converge requires an IC with an exact solution")
+        l_inf, l2 = summary["l_inf"], summary["l2"]
+        h = cfg.domain[0] / m
+        if prev is None:
+            order_linf = order_l2 = float("nan")
+        else:
+            ratio = math.log2(m / prev[0])
+            order_linf = math.log2(prev[1] / l_inf) / ratio if l_inf > 0 else float("inf")
+            order_l2 = math.log2(prev[2] / l2) / ratio if l2 > 0 else float("inf")
+        rows.append([m, h, l_inf, l2, order_linf, order_l2])
+        prev = (m, l_inf, l2)
+    csv_path = Path(cfg.out_dir) / "converge.csv"
+    _write_csv(csv_path, header, rows)
+    return {"status": "ok", "order_n": cfg.order_n, "rows": [dict(zip(header, r)) for r in rows],
+            "artifacts": {"converge_csv": str(csv_path)}}
