@@ -54,14 +54,14 @@ __device__ __forceinline__ void bulk_g2s(double* sdst, const double* gsrc, unsig
 }
 __device__ __forceinline__ void fence_proxy_async_smem() { asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory"); }
 
-template <int N_, int TX_, int TY_>
+template <int N_, int TX_, int TY_, int WARPS_ = 16, int STAGES_ = 3, int MINB_ = 1>
 struct Cfg {
     static constexpr int N = N_, n = N + 1, n2 = n * n, n3 = n2 * n, K2 = 2 * n;
     static constexpr int KS = K2 / 4;  // m8n8k4 k-steps per line
     static_assert(K2 % 4 == 0, "cell-pair form needs 2n divisible by 4");
     static_assert(n <= 8, "n outputs must fit the 8 MMA columns");
     static constexpr int TX = TX_, TY = TY_, NX = TX + 1, NY = TY + 1, NNODE = NX * NY;
-    static constexpr int WARPS = 16, THREADS = 32 * WARPS, STAGES = 3;
+    static constexpr int WARPS = WARPS_, THREADS = 32 * WARPS, STAGES = STAGES_, MINB = MINB_;
     static constexpr int UNS = n3;                   // U: dense node blocks [j3][j2][j1]
     static constexpr int WM = n2 + 1, WCS = n * WM;  // W: [node row][cell][m1][j3 j2], odd m1 stride
     static constexpr int VJ = n2 + 1, VCS = n * VJ;  // V: [cell][j3][m2 m1]
@@ -79,7 +79,7 @@ struct Cfg {
 }  // namespace cp5
 
 template <class C>
-__global__ void __launch_bounds__(C::THREADS, 1)
+__global__ void __launch_bounds__(C::THREADS, C::MINB)
 sep_fused_dmma_cp_kernel(const double* __restrict__ src, double* __restrict__ dst, Dims d, int off, int zchunk,
                          const __grid_constant__ SepOps<C::N> p, unsigned long long* first_bad,
                          const unsigned long long* guard) {
@@ -281,7 +281,10 @@ static int launch_cp(const double* src, double* dst, const Dims& d, const double
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM);
     if (e != cudaSuccess) return (int)e;
     const int64_t gx = (d.M1 + C::TX - 1) / C::TX, gy = (d.M2 + C::TY - 1) / C::TY;
-    const int64_t zchunk = choose_zchunk(gx * gy, nz, num_sms());  // one CTA per SM
+    int per_sm = 0;
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, C::THREADS, C::SMEM);
+    if (e != cudaSuccess) return (int)e;
+    const int64_t zchunk = choose_zchunk(gx * gy, nz, (int64_t)num_sms() * (per_sm > 0 ? per_sm : 1));
     const int64_t gz = (nz + zchunk - 1) / zchunk;
     kern<<<dim3((unsigned)gx, (unsigned)gy, (unsigned)gz), C::THREADS, C::SMEM, st>>>(src, dst, d, off, (int)zchunk,
                                                                                    ops, first_bad, guard);
@@ -290,6 +293,12 @@ static int launch_cp(const double* src, double* dst, const Dims& d, const double
 
 int sep_fused_dmma5_launch(const double* src, double* dst, const Dims& d, const double* A, int off, cudaStream_t st,
                            unsigned long long* first_bad, const unsigned long long* guard) {
+    static const int cfg = [] {
+        const char* e = getenv("H3_DMMA5_CFG");
+        return e ? atoi(e) : 0;
+    }();
+    if (cfg == 1) return launch_cp<cp5::Cfg<5, 4, 2, 8, 2, 2>>(src, dst, d, A, off, st, first_bad, guard);
+    if (cfg == 2) return launch_cp<cp5::Cfg<5, 4, 2, 8, 3, 1>>(src, dst, d, A, off, st, first_bad, guard);
     return launch_cp<cp5::Cfg<5, 4, 4>>(src, dst, d, A, off, st, first_bad, guard);
 }
 
