@@ -29,6 +29,7 @@
 #include <cstdlib>
 
 #include "h3_launch.h"
+#include "h3_tma.cuh"
 
 namespace h3 {
 
@@ -48,35 +49,13 @@ __device__ __forceinline__ void dmma_abl(double& d0, double& d1, double a, doubl
     }
 }
 
-// ---- TMA bulk copies + mbarriers (sm_90+) ----------------------------------------------
-__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count) : "memory");
-}
-__device__ __forceinline__ void mbar_fence_init() {
-    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
-}
-__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, unsigned bytes) {
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(bytes)
-                 : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
-    asm volatile(
-        "{\n.reg .pred p;\nWAIT_%=:\n"
-        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
-        "@!p bra WAIT_%=;\n}\n" ::"r"(smem_u32(bar)),
-        "r"(parity)
-        : "memory");
-}
-__device__ __forceinline__ void bulk_g2s(double* sdst, const double* gsrc, unsigned bytes, uint64_t* bar) {
-    asm volatile(
-        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
-            smem_u32(sdst)),
-        "l"(gsrc), "r"(bytes), "r"(smem_u32(bar))
-        : "memory");
-}
-__device__ __forceinline__ void fence_proxy_async_smem() {
-    asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
-}
+// TMA bulk copies + mbarriers: h3_tma.cuh
+using tma::bulk_g2s;
+using tma::fence_proxy_async_smem;
+using tma::mbar_arrive_expect_tx;
+using tma::mbar_fence_init;
+using tma::mbar_init;
+using tma::mbar_wait;
 
 // Tile / pipeline configuration of the DMMA kernel.
 // TMA: input planes arrive as one bulk copy per tile row (9 contiguous node blocks, split at
@@ -87,8 +66,8 @@ __device__ __forceinline__ void fence_proxy_async_smem() {
 template <int TY_, int WARPS_, int STAGES_, bool VALIAS_, int MINB_ = 1, int ABL_ = 0, bool TMA_ = false,
           bool LEAN_ = false, int PIPE_ = 0>
 struct Dm3Cfg {
-    // PIPE 1: x3 of plane p-1 shares a barrier interval with x1 of plane p (2 barriers/plane);
-    // PIPE 2: x3(p-2), x2(p-1) and x1(p) share one interval (1 barrier/plane, W and V doubled)
+    // PIPE 1: x3 of plane p-1 shares a barrier interval with x1 of plane p (2 barriers/plane).
+    // (A 1-barrier variant -- x3(p-2), x2(p-1), x1(p) with W and V doubled -- measured 17 % slower.)
     static constexpr int PIPE = PIPE_;
     static constexpr int ABL = ABL_;
     static constexpr bool TMA = TMA_;
@@ -112,7 +91,7 @@ struct Dm3Cfg {
     static constexpr size_t W_D = (size_t)NY * TX * WCS;
     static constexpr size_t V_D = (size_t)TY * TX * VCS;
     static constexpr size_t SMEM_DATA =
-        (STAGES * U_D + (PIPE == 2 ? 2 : 1) * W_D + (VALIAS ? 0 : (PIPE == 2 ? 2 : 1) * V_D)) * sizeof(double);
+        (STAGES * U_D + W_D + (VALIAS ? 0 : V_D)) * sizeof(double);
     static constexpr size_t SMEM = SMEM_DATA + (TMA ? STAGES * sizeof(uint64_t) : 0);
     static_assert(!TMA || NY <= WARPS, "one loader warp per tile row");
     static_assert(T3 % WARPS == 0, "x3 chains must divide evenly among warps");
@@ -133,7 +112,7 @@ sep_fused_dmma3_kernel(const double* __restrict__ src, double* __restrict__ dst,
     extern __shared__ __align__(16) unsigned char smem_raw[];
     double* U = reinterpret_cast<double*>(smem_raw);
     double* W = U + STAGES * C::U_D;
-    double* Vfix = W + (C::PIPE == 2 ? 2 : 1) * C::W_D;  // PIPE 2: W[2], then V[2]
+    double* Vfix = W + C::W_D;
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int q = lane & 3, g = lane >> 2, par = q >> 1;  // fragment coordinates
@@ -437,18 +416,7 @@ sep_fused_dmma3_kernel(const double* __restrict__ src, double* __restrict__ dst,
             issue();  // the stage it fills was last read before the barrier above
         }
     };
-    if constexpr (C::PIPE == 2) {
-        static_assert(!C::VALIAS, "PIPE keeps V(p-1) while stage p is refilled");
-        double* Wb[2] = {W, W + C::W_D};
-        double* Vb[2] = {Vfix, Vfix + C::V_D};
-        for (int pl = 0; pl <= P + 1; ++pl) {
-            if (pl < P) top(pl);
-            else __syncthreads();
-            if (pl >= 2) x3_pass(Vb[pl & 1], pl - 2);
-            if (pl >= 1 && pl <= P) x2_pass(Wb[(pl - 1) & 1], Vb[(pl - 1) & 1]);
-            if (pl < P) x1_pass(U + (pl % STAGES) * C::U_D, Wb[pl & 1]);
-        }
-    } else if constexpr (C::PIPE == 1) {
+    if constexpr (C::PIPE == 1) {
         static_assert(!C::VALIAS, "PIPE keeps V(p-1) while stage p is refilled");
         for (int pl = 0; pl <= P; ++pl) {
             if (pl < P) top(pl);
@@ -470,292 +438,6 @@ sep_fused_dmma3_kernel(const double* __restrict__ src, double* __restrict__ dst,
         }
     }
     cp_async_wait<0>();
-}
-
-// ---------------------------------------------------------------------------------------
-// v2 (H3_DMMA_CFG=9): same tile march and MMA schedule, outputs leave through shared memory.
-// Measured equal to v1 (32.1 vs 31.8 ms at 512^3): the x3 store instructions are not the limiter.
-//  * x1 / x2 as in v1.  (Storing after every MMA -- pending lanes writing partials that the
-//    same lane overwrites one node later -- removes the value selects but doubles the shared
-//    stores; measured slower, 37.5 vs 33.9 ms at 512^3.)
-//  * x3: finished cell planes are staged in shared memory (2 slots, written by the
-//    completing lanes only) and leave with one TMA bulk copy
-//    (cp.async.bulk) per tile row -- 8 contiguous node blocks = 4 KB -- instead of
-//    per-lane 8-byte stores with 64-bit address arithmetic.
-// ---------------------------------------------------------------------------------------
-__device__ __forceinline__ void bulk_s2g(double* gdst, const double* ssrc, uint32_t bytes) {
-    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;\n" ::"l"(gdst),
-                 "r"(smem_u32(ssrc)), "r"(bytes)
-                 : "memory");
-}
-__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;\n" ::: "memory"); }
-__device__ __forceinline__ void bulk_wait_read1() { asm volatile("cp.async.bulk.wait_group.read 1;\n" ::: "memory"); }
-__device__ __forceinline__ void bulk_wait0() { asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory"); }
-__device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory"); }
-// exponent field all ones: Inf or NaN
-__device__ __forceinline__ bool special(double v) {
-    return (__double2hiint(v) & 0x7ff00000) == 0x7ff00000;
-}
-
-template <int TY_, int STAGES_>
-struct Dm3v2Cfg {
-    static constexpr int ABL = 0;
-    static constexpr int n = 4, n3 = 64;
-    static constexpr int TX = 8, TY = TY_, NX = TX + 1, NY = TY + 1, NCOL = NX * NY;
-    static constexpr int WARPS = 16, THREADS = 512, STAGES = STAGES_;
-    static constexpr int UNS = 64;
-    static constexpr int WRS = 20, WCS = 80;
-    static constexpr int VRS = 17, VCS = 68;
-    static constexpr int T3 = 2 * TX * TY, K3 = T3 / WARPS;
-    static constexpr int CPW = (NCOL + WARPS - 1) / WARPS;
-    static constexpr size_t U_D = (size_t)NCOL * UNS;
-    static constexpr size_t W_D = (size_t)NY * TX * WCS;
-    static constexpr size_t V_D = (size_t)TY * TX * VCS;
-    static constexpr size_t O_D = (size_t)TY * TX * n3;  // one staged output cell plane
-    static constexpr size_t SMEM = (STAGES * U_D + W_D + 2 * O_D) * sizeof(double);
-    static_assert(2 * NY == WARPS && 2 * TX == WARPS, "one x1 and one x2 chain per warp");
-    static_assert(T3 % WARPS == 0, "x3 chains must divide evenly among warps");
-    static_assert(V_D <= U_D, "V aliases the consumed input stage");
-    static_assert(NX % 2 == 1, "x1 edge handling assumes an even last node index");
-};
-
-template <class C>
-__global__ void __launch_bounds__(C::THREADS, 1)
-sep_fused_dmma3v2_kernel(const double* __restrict__ src, double* __restrict__ dst, Dims d, int off,
-                         int zchunk, const __grid_constant__ SepOps<3> p,
-                         unsigned long long* first_bad, const unsigned long long* guard) {
-    constexpr int n3 = C::n3, TX = C::TX, TY = C::TY, NX = C::NX, NY = C::NY;
-    constexpr int NCOL = C::NCOL, WARPS = C::WARPS, STAGES = C::STAGES, UNS = C::UNS;
-    constexpr int WRS = C::WRS, WCS = C::WCS, VRS = C::VRS, VCS = C::VCS, K3 = C::K3;
-    if (guarded_out(guard, first_bad)) return;
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    double* U = reinterpret_cast<double*>(smem_raw);
-    double* W = U + STAGES * C::U_D;
-    double* OUT = W + C::W_D;
-
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int q = lane & 3, g = lane >> 2, par = q >> 1;  // fragment coordinates
-    const int M1 = (int)d.M1, M2 = (int)d.M2;
-    const int cx0 = blockIdx.x * TX, cy0 = blockIdx.y * TY;
-    const int64_t zc0 = d.z_begin + (int64_t)blockIdx.z * zchunk;
-    const int64_t zc1 = min(zc0 + (int64_t)zchunk, d.z_end);
-    const int P = (int)(zc1 - zc0) + 1;
-    const int64_t plane_elems = (int64_t)M1 * M2 * n3;
-
-    double bop[3][2];
-#pragma unroll
-    for (int ax = 0; ax < 3; ++ax) {
-        const int m = g & 3, hi = g >> 2;
-        bop[ax][0] = hi ? p.A[ax][m][4 + q] : p.A[ax][m][q];
-        bop[ax][1] = hi ? p.A[ax][m][q] : p.A[ax][m][4 + q];
-    }
-
-    int nodeoff[C::CPW];
-#pragma unroll
-    for (int j = 0; j < C::CPW; ++j) {
-        const int c = min(warp + WARPS * j, NCOL - 1);
-        const int ly = c / NX, lx = c - (c / NX) * NX;
-        int gx = cx0 + off + lx, gy = cy0 + off + ly;
-        gx %= M1; if (gx < 0) gx += M1;
-        gy %= M2; if (gy < 0) gy += M2;
-        nodeoff[j] = (gy * M1 + gx) * n3 + 2 * lane;
-    }
-    int64_t gz_next = d.periodic_z ? wrap(zc0 + off, d.M3) : zc0 + off;
-    int issued = 0;
-    auto issue = [&]() {
-        if (issued < P) {
-            const double* base = src + gz_next * plane_elems;
-            double* Ub = U + (issued % STAGES) * C::U_D + 2 * lane;
-#pragma unroll
-            for (int j = 0; j < C::CPW; ++j)
-                if (NCOL % WARPS == 0 || warp + WARPS * j < NCOL)
-                    cp_async16(Ub + (warp + WARPS * j) * UNS, base + nodeoff[j]);
-            ++gz_next;
-            if (d.periodic_z && gz_next == d.M3) gz_next = 0;
-            ++issued;
-        }
-        cp_async_commit();
-    };
-#pragma unroll
-    for (int s = 0; s < STAGES - 1; ++s) issue();
-
-    // bulk row stores of a finished cell plane (warp 0, one lane per tile row)
-    const int row_cells = min(TX, M1 - cx0);
-    auto store_plane = [&](int cplane, int slot) {
-        if (warp == 0 && lane < TY && cy0 + lane < M2) {
-            const int64_t node = ((zc0 + cplane) * M2 + cy0 + lane) * (int64_t)M1 + cx0;
-            bulk_s2g(dst + node * n3, OUT + slot * C::O_D + lane * TX * n3, (uint32_t)(row_cells * n3 * 8));
-        }
-        if (warp == 0) bulk_commit();
-    };
-
-    // x1 chain: warp -> (row ly, line-half h); x2 chain: warp -> (column ix, line-half h)
-    const int h = warp & 1, L = 8 * h + g;
-    const int ly1 = warp >> 1, ix2 = warp >> 1;
-    // x3 chains: t = warp + WARPS k -> (cell t >> 1, half t & 1); lane's slot offset per chain
-    int opos[K3];
-    bool olive[K3];
-#pragma unroll
-    for (int k = 0; k < K3; ++k) {
-        const int t = warp + WARPS * k;
-        const int cell = t >> 1, hh = t & 1;
-        opos[k] = cell * n3 + (2 * (q & 1)) * 16 + 8 * hh + g;
-        olive[k] = cx0 + (cell % TX) < M1 && cy0 + cell / TX < M2;
-    }
-    double acc[K3][2];
-#pragma unroll
-    for (int k = 0; k < K3; ++k) acc[k][0] = acc[k][1] = 0.0;
-
-    for (int pl = 0; pl < P; ++pl) {
-        cp_async_wait<STAGES - 2>();
-        __syncthreads();
-        issue();
-        if (pl >= 2) store_plane(pl - 2, pl & 1);  // finished at the previous iteration's x3
-        const double* Ub = U + (pl % STAGES) * C::U_D;
-        double* V = U + (pl % STAGES) * C::U_D;  // x2 output reuses the consumed input stage
-
-        // ---- x1 ------------------------------------------------------------------------------
-        {
-            const double* ua = Ub + ly1 * NX * UNS + L * 4 + q;
-            double* wl = W + ly1 * TX * WCS + (2 * h + (g >> 2)) * WRS + (g & 3) + (2 * (q & 1)) * 4;
-            double a[NX];
-#pragma unroll
-            for (int lx = 0; lx < NX; ++lx) a[lx] = ua[lx * UNS];
-            double r0 = 0.0, r1 = 0.0;
-                // an even cell's values are held one node longer so both halves store together
-                double sv0 = 0.0, sv1 = 0.0;
-#pragma unroll
-                for (int lx = 0; lx < NX; ++lx) {
-                    dmma_abl<C::ABL>(r0, r1, a[lx], bop[0][lx & 1]);
-                    if (lx & 1) {
-                        sv0 = r0;
-                        sv1 = r1;
-                    } else if (lx > 0) {
-                        double* w = wl + (lx - 1 - (par ^ 1)) * WCS;
-                        w[0] = par ? r0 : sv0;
-                        w[4] = par ? r1 : sv1;
-                    }
-                    const bool done = par == ((lx + 1) & 1);
-                    r0 = done ? 0.0 : r0;
-                    r1 = done ? 0.0 : r1;
-                }
-        }
-        __syncthreads();
-
-        // ---- x2 ------------------------------------------------------------------------------
-        {
-            const double* wa = W + ix2 * WCS + (L >> 2) * WRS + (L & 3) * 4 + q;
-            double* vl = V + ix2 * VCS + (L & 3) * 4 + (L >> 2) + (2 * (q & 1)) * VRS;
-            double a[NY];
-#pragma unroll
-            for (int ly = 0; ly < NY; ++ly) a[ly] = wa[ly * TX * WCS];
-            double r0 = 0.0, r1 = 0.0;
-                double sv0 = 0.0, sv1 = 0.0;
-#pragma unroll
-                for (int ly = 0; ly < NY; ++ly) {
-                    dmma_abl<C::ABL>(r0, r1, a[ly], bop[1][ly & 1]);
-                    const bool done = par == ((ly + 1) & 1);
-                    if (ly & 1) {
-                        if (ly == NY - 1) {  // lone last cell row: half-warp store
-                            if (done) {
-                                double* v = vl + (ly - 1) * TX * VCS;
-                                v[0] = r0;
-                                v[VRS] = r1;
-                            }
-                        } else {
-                            sv0 = r0;
-                            sv1 = r1;
-                        }
-                    } else if (ly > 0) {
-                        double* v = vl + (ly - 1 - (par ^ 1)) * TX * VCS;
-                        v[0] = par ? r0 : sv0;
-                        v[VRS] = par ? r1 : sv1;
-                    }
-                    r0 = done ? 0.0 : r0;
-                    r1 = done ? 0.0 : r1;
-                }
-        }
-        // the slot this x3 writes was last bulk-stored at the previous iteration: let that copy
-        // finish reading (the one issued at this iteration may stay in flight)
-        if (pl >= 3 && warp == 0) bulk_wait_read1();
-        __syncthreads();
-
-        // ---- x3 ------------------------------------------------------------------------------
-        {
-            double* slot = OUT + ((pl + 1) & 1) * C::O_D;  // finished cell plane pl - 1
-            // non-finite screen: min over (~hi & exponent mask) is 0 iff some value is Inf/NaN
-            unsigned screen = 0x7ff00000u;
-#pragma unroll
-            for (int k = 0; k < K3; ++k) {
-                const int t = warp + WARPS * k;
-                const int cell = t >> 1, hh = t & 1;
-                const int LL = 8 * hh + g;
-                const double a = V[cell * VCS + (LL >> 2) * VRS + (LL & 3) * 4 + q];
-                const int ph = (pl + k) & 1;
-                dmma_abl<C::ABL>(acc[k][0], acc[k][1], a, ph ? bop[2][1] : bop[2][0]);
-                const bool done = par == ((pl + k + 1) & 1);
-                double* o = slot + opos[k];
-                if (done) {
-                    o[0] = acc[k][0];
-                    o[16] = acc[k][1];
-                }
-                screen = min(screen, min(~(unsigned)__double2hiint(acc[k][0]) & 0x7ff00000u,
-                                         ~(unsigned)__double2hiint(acc[k][1]) & 0x7ff00000u));
-                acc[k][0] = done ? 0.0 : acc[k][0];
-                acc[k][1] = done ? 0.0 : acc[k][1];
-            }
-            if (pl > 0 && screen == 0u) {  // rare: locate the first bad node of this plane
-#pragma unroll
-                for (int k = 0; k < K3; ++k) {
-                    const bool done = par == ((pl + k + 1) & 1);
-                    const double* o = slot + opos[k];
-                    if (done && olive[k] && (special(o[0]) || special(o[16]))) {
-                        const int cell = (warp + WARPS * k) >> 1;
-                        flag_bad(first_bad, ((zc0 + pl - 1) * M2 + cy0 + cell / TX) * (int64_t)M1 + cx0 + cell % TX);
-                    }
-                }
-            }
-        }
-        fence_async_smem();  // make this thread's staged outputs visible to the bulk copies
-    }
-    __syncthreads();
-    if (P >= 2) store_plane(P - 2, P & 1);
-    if (warp == 0) bulk_wait0();
-    cp_async_wait<0>();
-}
-
-template <class C>
-static int launch_dm3v2(const double* src, double* dst, const Dims& d, const SepOps<3>& ops, int off,
-                        cudaStream_t st, unsigned long long* first_bad, const unsigned long long* guard) {
-    const int64_t nz = d.z_end - d.z_begin;
-    auto kern = sep_fused_dmma3v2_kernel<C>;
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM);
-    if (e != cudaSuccess) return (int)e;
-    const int64_t gx = (d.M1 + C::TX - 1) / C::TX, gy = (d.M2 + C::TY - 1) / C::TY;
-    const int64_t zchunk = choose_zchunk(gx * gy, nz, num_sms());  // one CTA per SM
-    const int64_t gz = (nz + zchunk - 1) / zchunk;
-    static const int cy = [] {
-        const char* s = getenv("H3_DMMA_CLUSTER_Y");
-        return s ? atoi(s) : 2;
-    }();
-    if (cy > 1 && gy % cy == 0) {
-        cudaLaunchConfig_t lc = {};
-        lc.gridDim = dim3((unsigned)gx, (unsigned)gy, (unsigned)gz);
-        lc.blockDim = dim3(C::THREADS);
-        lc.dynamicSmemBytes = C::SMEM;
-        lc.stream = st;
-        cudaLaunchAttribute at[1];
-        at[0].id = cudaLaunchAttributeClusterDimension;
-        at[0].val.clusterDim.x = 1;
-        at[0].val.clusterDim.y = cy;
-        at[0].val.clusterDim.z = 1;
-        lc.attrs = at;
-        lc.numAttrs = 1;
-        return (int)cudaLaunchKernelEx(&lc, kern, src, dst, d, off, (int)zchunk, ops, first_bad, guard);
-    }
-    kern<<<dim3((unsigned)gx, (unsigned)gy, (unsigned)gz), C::THREADS, C::SMEM, st>>>(
-        src, dst, d, off, (int)zchunk, ops, first_bad, guard);
-    return (int)cudaGetLastError();
 }
 
 template <class C>
@@ -821,15 +503,9 @@ int sep_fused_dmma3_launch(const double* src, double* dst, const Dims& d, const 
     switch (cfg) {
         // measurement variants (tools/time_fused.py with H3_DMMA_CFG=k)
         case 6: return launch_dm3<Dm3Cfg<7, 16, 3, true>>(src, dst, d, ops, off, st, first_bad, guard);  // cp.async loads
-        case 9: return launch_dm3v2<Dm3v2Cfg<7, 3>>(src, dst, d, ops, off, st, first_bad, guard);  // bulk stores
         case 11: return launch_dm3<Dm3Cfg<7, 16, 3, true, 1, 1, true>>(src, dst, d, ops, off, st, first_bad, guard);
         case 14: return launch_dm3<Dm3Cfg<7, 16, 3, true, 1, 4, true>>(src, dst, d, ops, off, st, first_bad, guard);
         case 15: return launch_dm3<Dm3Cfg<7, 16, 3, true, 1, 5, true>>(src, dst, d, ops, off, st, first_bad, guard);
-        case 20: return launch_dm3<Dm3Cfg<7, 16, 3, true, 1, 0, true, true>>(src, dst, d, ops, off, st, first_bad, guard);
-        case 22: return launch_dm3<Dm3Cfg<3, 8, 3, true, 2, 0, true>>(src, dst, d, ops, off, st, first_bad, guard);
-        case 25: return launch_dm3<Dm3Cfg<7, 16, 3, false, 1, 0, true, false, 1>>(src, dst, d, ops, off, st, first_bad, guard);
-        case 27: return launch_dm3<Dm3Cfg<6, 16, 3, false, 1, 0, true, true, 2>>(src, dst, d, ops, off, st, first_bad, guard);
-        case 28: return launch_dm3<Dm3Cfg<6, 16, 3, false, 1, 0, true, true, 1>>(src, dst, d, ops, off, st, first_bad, guard);
         case 16: return launch_dm3<Dm3Cfg<7, 16, 3, true, 1, 0, true>>(src, dst, d, ops, off, st, first_bad, guard);
         // default: TMA row loads, x3(p-1) pipelined with x1(p) (2 barriers per plane), lean x3 stores
         default: return launch_dm3<Dm3Cfg<7, 16, 3, false, 1, 0, true, true, 1>>(src, dst, d, ops, off, st, first_bad, guard);
