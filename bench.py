@@ -55,6 +55,8 @@ def parse():
     ap.add_argument("--no-extras", action="store_true",
                     help="skip the secondary configs (two-kernel 512^3 / 128^3, m=5 256^3)")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    ap.add_argument("--backend", default="nccl", choices=["nccl", "gloo"],
+                    help="process-group backend for N>1 (gloo: test the multi-rank path on one GPU)")
     return ap.parse_args()
 
 
@@ -173,6 +175,9 @@ def cpu_sample_cells(order_n):
 def run_reference(args, rank, world):
     if rank != 0:
         return
+    # torchrun exports OMP_NUM_THREADS=1 per rank; the reference arm uses every host core it
+    # can (set before the oracle's OpenMP runtime starts: torch is not imported on this arm)
+    os.environ["OMP_NUM_THREADS"] = str(len(os.sched_getaffinity(0)))
     order_n = args.order
     cells = cpu_sample_cells(order_n)
     rates = []
@@ -214,9 +219,12 @@ def main():
     import paper_1609_09841_b200 as hb
     from paper_1609_09841_b200 import _native, distributed as hd
 
-    torch.cuda.set_device(local)
+    torch.cuda.set_device(local % torch.cuda.device_count())
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if args.backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group("gloo")
     order_n, m = args.order, args.cells
     n3 = (order_n + 1) ** 3
     peak_gbs, peak_src = peaks()
@@ -259,7 +267,7 @@ def main():
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
-    with ClockSampler(local) as clocks:
+    with ClockSampler(local % torch.cuda.device_count()) as clocks:
         kernel_events.clear()
         torch.cuda.synchronize()
         if world > 1:
@@ -274,7 +282,7 @@ def main():
         if world > 1:
             dist.barrier()
         ms = t0.elapsed_time(t1)
-    ms_t = torch.tensor([ms], dtype=torch.float64, device="cuda")
+    ms_t = torch.tensor([ms], dtype=torch.float64, device="cuda" if args.backend == "nccl" else "cpu")
     if world > 1:
         dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
     ms_max = float(ms_t.item())

@@ -68,6 +68,15 @@ def exchange_halo(buf: torch.Tensor, off: int, group=None, async_op: bool = Fals
         return []
     to_g = dist.get_global_rank(group, send_to) if group is not None else send_to
     from_g = dist.get_global_rank(group, recv_from) if group is not None else recv_from
+    if buf.is_cuda and dist.get_backend(group) == "gloo":
+        # gloo moves host tensors only: stage the planes (used to test the multi-rank GPU path
+        # on one device; production runs use NCCL over NVLink)
+        send, recv = buf[send_i].cpu(), torch.empty_like(buf[recv_i], device="cpu")
+        for w in dist.batch_isend_irecv([dist.P2POp(dist.isend, send, to_g, group),
+                                         dist.P2POp(dist.irecv, recv, from_g, group)]):
+            w.wait()
+        buf[recv_i].copy_(recv)
+        return []
     ops = [dist.P2POp(dist.isend, buf[send_i], to_g, group),
            dist.P2POp(dist.irecv, buf[recv_i], from_g, group)]
     works = dist.batch_isend_irecv(ops)
