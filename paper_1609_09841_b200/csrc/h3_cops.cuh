@@ -6,9 +6,10 @@
 // std::integral_constant<int, 0..K-1> so operator offsets are compile-time constants.
 //
 // Host side: cop_acquire() returns a slot holding the requested operator set (uploading it with
-// cudaMemcpyToSymbolAsync on the caller's stream when no slot matches); cop_release() records
-// the launch's completion event on the slot.  A slot is overwritten only after every recorded
-// user has completed (the uploading stream waits on their events).
+// cudaMemcpyToSymbolAsync on the caller's stream when no slot matches, then recording the slot's
+// `ready` event; a caller on another stream that finds the slot waits on that event);
+// cop_release() records the launch's completion event on the slot.  A slot is overwritten only
+// after every recorded user has completed (the uploading stream waits on their events).
 #pragma once
 #include <cuda_runtime.h>
 
@@ -52,6 +53,7 @@ struct CopSlotState {
     int count = -1;
     double bits[COP_SLOT];
     std::vector<cudaEvent_t> users;
+    cudaEvent_t ready = nullptr;  // recorded after the upload; other streams wait on it
 };
 struct CopDeviceState {
     CopSlotState slot[COP_SLOTS];
@@ -79,6 +81,11 @@ static int cop_acquire(const double* ops, int count, cudaStream_t st, int* slot)
     CopDeviceState& D = cop_device(dev);
     for (int s = 0; s < COP_SLOTS; ++s)
         if (D.slot[s].count == count && std::memcmp(D.slot[s].bits, ops, count * sizeof(double)) == 0) {
+            // the upload may still be queued on another stream: order this stream after it
+            if (D.slot[s].ready) {
+                e = cudaStreamWaitEvent(st, D.slot[s].ready, 0);
+                if (e != cudaSuccess) return (int)e;
+            }
             *slot = s;
             return 0;
         }
@@ -94,6 +101,12 @@ static int cop_acquire(const double* ops, int count, cudaStream_t st, int* slot)
     S.count = -1;
     e = cudaMemcpyToSymbolAsync(h3_cop, ops, count * sizeof(double), (size_t)s * COP_SLOT * sizeof(double),
                                 cudaMemcpyHostToDevice, st);
+    if (e != cudaSuccess) return (int)e;
+    if (!S.ready) {
+        e = cudaEventCreateWithFlags(&S.ready, cudaEventDisableTiming);
+        if (e != cudaSuccess) return (int)e;
+    }
+    e = cudaEventRecord(S.ready, st);
     if (e != cudaSuccess) return (int)e;
     std::memcpy(S.bits, ops, count * sizeof(double));
     S.count = count;
