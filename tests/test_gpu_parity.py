@@ -390,3 +390,36 @@ def test_constant_operator_ring_many_operator_sets():
     torch.cuda.synchronize()
     for a, b in zip(outs, refs):
         assert rm.rel_err(a.cpu().numpy(), b.cpu().numpy()) <= 1e-13
+
+
+def test_constant_operator_ring_cross_stream_upload_order():
+    """An operator set uploaded on a busy stream and reused at once on another stream: the
+    second stream must wait for the upload (slot `ready` event), not read stale constants."""
+    n = 2
+    nn = n + 1
+    src = torch.from_numpy(np.random.default_rng(5).uniform(-1, 1, (4, 5, 6, nn, nn, nn))).cuda()
+    base = np.ascontiguousarray(rm.interp_matrix(n))
+    a, b = torch.cuda.Stream(), torch.cuda.Stream()
+    lib = _native.lib()
+    for k in range(6):  # cycle through more sets than slots so every set is a fresh upload
+        h = np.ascontiguousarray(base * (1.0 + 0.37 * (k + 1)))
+        outs = []
+        for st in (a, b):
+            st.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(a):
+            torch.cuda._sleep(2_000_000)  # keep stream a busy so its upload is queued late
+        for st in (a, b):
+            coeff = torch.empty((4, 5, 6, 6, 6, 6), dtype=torch.float64, device="cuda")
+            rc = lib.h3_recon_pass(ctypes.c_void_p(src.data_ptr()), ctypes.c_void_p(coeff.data_ptr()),
+                                   6, 5, 4, n, h.ctypes.data_as(ctypes.c_void_p), 0, 0, 4, 1,
+                                   _native.VARIANTS["separable"], ctypes.c_void_p(st.cuda_stream), None)
+            assert rc == 0
+            outs.append(coeff)
+        ref = torch.empty_like(outs[0])
+        rc = lib.h3_recon_pass(ctypes.c_void_p(src.data_ptr()), ctypes.c_void_p(ref.data_ptr()), 6, 5, 4, n,
+                               h.ctypes.data_as(ctypes.c_void_p), 0, 0, 4, 1, _native.VARIANTS["literal"],
+                               None, None)
+        assert rc == 0
+        torch.cuda.synchronize()
+        for o in outs:
+            assert rm.rel_err(o.cpu().numpy(), ref.cpu().numpy()) <= 1e-13
