@@ -27,7 +27,7 @@ import numpy as np
 import torch
 
 from . import perf
-from .field import DofField, GridSpec, write_snapshot
+from .field import DofField, GridSpec, read_snapshot, write_snapshot
 from .pipeline import AllocationStats, InstabilityError, OperatorSet, StepConfig, _new_flags, _node_of, half_step, \
     select_dt
 from .problems import Constant, FourierMode, Monomial, SeparableIC, error_norms_async, exact_solution, init_field, \
@@ -58,6 +58,7 @@ class RunConfig:
     ic: tuple = dc_field(default_factory=lambda: ({"kind": "plane_wave"},))
     seed: int = 0
     out_dir: str = "out"
+    resume: str | None = None  # snapshot base path: continue from its field and time
 
     def __post_init__(self):
         cells = (self.cells,) * 3 if isinstance(self.cells, int) else tuple(self.cells)
@@ -159,7 +160,17 @@ def execute_run(cfg: RunConfig, write_artifacts: bool = True) -> dict:
     grid = GridSpec(cfg.cells, cfg.domain, "primary")
     ops = OperatorSet.for_grid(grid, cfg.order_n)
     ic = build_ic(cfg)
-    state = init_field(ic, grid, cfg.order_n, precision=cfg.precision)
+    t0 = 0.0
+    if cfg.resume:
+        # resume path: the snapshot's field and time, same grid and order
+        state, t0 = read_snapshot(cfg.resume)
+        if (state.grid.cells_per_axis, state.grid.domain_lengths, state.order_n, state.grid.parity) != \
+                (grid.cells_per_axis, grid.domain_lengths, cfg.order_n, "primary"):
+            raise ConfigError("resume: snapshot grid/order does not match the run configuration")
+        if state.precision != cfg.precision:
+            raise ConfigError("resume: snapshot precision does not match the run configuration")
+    else:
+        state = init_field(ic, grid, cfg.order_n, precision=cfg.precision)
     scratch = DofField.zeros(grid.with_parity("dual"), cfg.order_n, precision=cfg.precision)
     n_steps, dt = _plan_steps(cfg, grid, step_cfg)
     track = ic.smoothness_class == "analytic" and cfg.precision == "double"
@@ -170,7 +181,7 @@ def execute_run(cfg: RunConfig, write_artifacts: bool = True) -> dict:
     stream = torch.cuda.current_stream(dev)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     if track:
-        error_norms_async(state, exact_solution(ic, 0.0, grid.domain_lengths), norms[0])
+        error_norms_async(state, exact_solution(ic, t0, grid.domain_lengths), norms[0])
     e0.record(stream)
     prev = None
     for k in range(n_steps):
@@ -181,19 +192,19 @@ def execute_run(cfg: RunConfig, write_artifacts: bool = True) -> dict:
                   _check=False)
         prev = f1
         if track:
-            error_norms_async(state, exact_solution(ic, (k + 1) * dt, grid.domain_lengths), norms[k + 1])
+            error_norms_async(state, exact_solution(ic, t0 + (k + 1) * dt, grid.domain_lengths), norms[k + 1])
     e1.record(stream)
     host_flags = flags.cpu().numpy()  # one synchronisation for the whole run
     for i, bad in enumerate(host_flags):
         if int(bad) != -1:
             raise InstabilityError(node=_node_of(int(bad), (scratch.grid, state.grid)[i % 2]), step=i // 2 + 1)
     wall = e0.elapsed_time(e1) / 1e3
-    t = n_steps * dt
+    t = t0 + n_steps * dt
     h1, h2, h3 = grid.spacings
     error_rows = []
     if track:
         for k, (linf, sumsq) in enumerate(norms.cpu().tolist()):
-            error_rows.append([k, k * dt, linf, math.sqrt(h1 * h2 * h3 * sumsq)])
+            error_rows.append([k, t0 + k * dt, linf, math.sqrt(h1 * h2 * h3 * sumsq)])
     result = {"status": "ok", "steps": n_steps, "dt": dt, "final_time": t, "mode": cfg.mode,
               "order_n": cfg.order_n, "seconds": wall, "peak_aux_bytes": stats.peak_aux_bytes, "artifacts": {}}
     if track:

@@ -88,3 +88,21 @@ def test_execute_run_separable_default_close_to_reference(tmp_path):
     row = GOLD["runs"][0]
     s = runner.execute_run(runner.RunConfig(out_dir=str(tmp_path), **row["config"]), write_artifacts=False)
     assert s["l_inf"] == pytest.approx(row["summary"]["l_inf"], rel=1e-2)
+
+
+@pytest.mark.gpu
+def test_resume_from_snapshot_continues_the_run(tmp_path):
+    """10 steps == 4 steps, snapshot, resume for 6 more (bit-identical field, same errors)."""
+    base = dict(order_n=3, cells=(12, 10, 8), variant="literal")
+    full = runner.execute_run(runner.RunConfig(steps=10, out_dir=str(tmp_path / "full"), **base))
+    first = runner.execute_run(runner.RunConfig(steps=4, out_dir=str(tmp_path / "a"), **base))
+    snap = str(Path(first["artifacts"]["snapshot_bin"]).with_suffix(""))
+    second = runner.execute_run(runner.RunConfig(steps=6, out_dir=str(tmp_path / "b"), resume=snap, **base))
+    assert second["final_time"] == pytest.approx(full["final_time"], rel=1e-15)
+    assert second["l_inf"] == pytest.approx(full["l_inf"], rel=1e-12)
+    a = Path(full["artifacts"]["snapshot_bin"]).read_bytes()
+    b = Path(second["artifacts"]["snapshot_bin"]).read_bytes()
+    assert a == b
+    with pytest.raises(runner.ConfigError, match="resume"):
+        runner.execute_run(runner.RunConfig(steps=1, out_dir=str(tmp_path / "c"), resume=snap,
+                                            order_n=3, cells=(12, 10, 9)))
