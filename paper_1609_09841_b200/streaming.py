@@ -5,7 +5,7 @@ drop-in equivalent with host buffers has to move the whole primary field to the 
 every step; done naively (upload, step, download) that is two serial PCIe transfers per step.
 `HostStepper` pipelines them instead: the primary field is cut into x3 chunks and, per step,
 
-    upload chunk k (+ the first plane of chunk k+1)          -> stream h2d
+    upload chunk k                                            -> stream h2d
     dual chunk k      = half step off=0 of those planes       -> stream compute
     primary chunk k   = half step off=-1 of dual chunks k-1,k -> stream compute
     download primary chunk k                                  -> stream d2h
@@ -16,7 +16,9 @@ so grids larger than HBM (e.g. 1024^3 at m = 3, 550 GB per field) can be stepped
 
 Wrap-around (periodic x3): dual chunk K-1 needs primary plane 0, and primary chunk 0 needs dual
 plane M3-1, so primary chunk 0 is finished last; its dual chunk is kept in a dedicated buffer
-and the original plane 0 is uploaded with chunk K-1 before chunk 0 is written back.
+and a device copy of the original plane 0 serves as the ghost of chunk K-1.  The other ghost
+planes are copied device to device from the next chunk's upload, so every primary plane crosses
+PCIe exactly once in each direction.
 
 Each chunk is a slab with ghost planes, stepped by the same C-ABI half step as the
 single-field path (h3_fused_pass with periodic_z = 0), so results are bit-identical to
@@ -82,10 +84,11 @@ class HostStepper:
         self.dbuf = [torch.empty(shape(cmax + 1), **kw) for _ in range(2)]   # ghost + dual chunk
         self.dual0 = torch.empty(shape(self.chunks[0][1] + 1), **kw)         # dual chunk 0 (kept)
         self.pout = [torch.empty(shape(cmax), **kw) for _ in range(2)]
+        self.plane0 = torch.empty(shape(1)[1:], **kw)
         self.s_h2d = torch.cuda.Stream(self.device)
         self.s_cmp = torch.cuda.Stream(self.device)
         self.s_d2h = torch.cuda.Stream(self.device)
-        self.h2d_bytes = m3 * plane * 8 + len(self.chunks) * plane * 8
+        self.h2d_bytes = m3 * plane * 8
         self.d2h_bytes = m3 * plane * 8
         self._plane = plane
 
@@ -124,7 +127,8 @@ class HostStepper:
                 if pin_free[k % 2] is not None:
                     self.s_h2d.wait_event(pin_free[k % 2])
                 buf[:L].copy_(self.host[z0:z1], non_blocking=nb)
-                buf[L].copy_(self.host[z1 % m3], non_blocking=nb)
+                if k == 0:  # original plane 0: the ghost of the last dual chunk (wrap)
+                    self.plane0.copy_(buf[0])
                 e = ev()
                 e.record(self.s_h2d)
             return e
@@ -155,6 +159,13 @@ class HostStepper:
             dst = self.dual0 if k == 0 else self.dbuf[k % 2]
             with torch.cuda.stream(self.s_cmp):
                 self.s_cmp.wait_event(up)
+                # high ghost plane = first plane of chunk k+1 (already on the device), or the
+                # original plane 0 for the last chunk: each primary plane crosses PCIe once
+                if nxt is not None:
+                    self.s_cmp.wait_event(nxt)
+                    self.pin[k % 2][L].copy_(self.pin[(k + 1) % 2][0])
+                else:
+                    self.pin[k % 2][L].copy_(self.plane0)
                 self._half(self.pin[k % 2], dst[1:], L, 0, fac, flags[0, k])
                 e = ev()
                 e.record(self.s_cmp)
