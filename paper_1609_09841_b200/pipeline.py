@@ -225,13 +225,22 @@ def _variant_code(cfg: StepConfig, precision: str) -> int:
     return _native.VARIANTS[cfg.variant]
 
 
-def _coeff_chunk_planes(grid: GridSpec, order_n: int, itemsize: int, budget: int | None) -> int:
+_CHUNK_CACHE: dict = {}
+
+
+def _coeff_chunk_planes(grid: GridSpec, order_n: int, itemsize: int, budget: int | None,
+                        refresh: bool = False) -> int:
+    """x3 planes of the two-pass coefficient field that fit the budget (default: 85 % of the free
+    HBM minus 1 GiB).  The free-memory query (~65 us) is cached per grid; `refresh` re-queries."""
     m1, m2, m3 = grid.cells_per_axis
     s = 2 * order_n + 2
     per_plane = m1 * m2 * s ** 3 * itemsize
     if budget is None:
-        free, _total = torch.cuda.mem_get_info()
-        budget = max(per_plane, int(0.85 * free) - (1 << 30))
+        key = (grid.cells_per_axis, order_n, itemsize, torch.cuda.current_device())
+        if refresh or key not in _CHUNK_CACHE:
+            free, _total = torch.cuda.mem_get_info()
+            _CHUNK_CACHE[key] = max(per_plane, int(0.85 * free) - (1 << 30))
+        budget = _CHUNK_CACHE[key]
     return max(1, min(m3, budget // per_plane))
 
 
@@ -302,7 +311,12 @@ def half_step(
         else:
             s = ops.side
             chunk = _coeff_chunk_planes(src.grid, order_n, src.tensor.element_size(), cfg.coeff_budget_bytes)
-            coeff = torch.empty((chunk, m2, m1, s, s, s), dtype=src.tensor.dtype, device=device)
+            try:
+                coeff = torch.empty((chunk, m2, m1, s, s, s), dtype=src.tensor.dtype, device=device)
+            except torch.OutOfMemoryError:  # free memory shrank since the cached query
+                chunk = _coeff_chunk_planes(src.grid, order_n, src.tensor.element_size(), cfg.coeff_budget_bytes,
+                                            refresh=True)
+                coeff = torch.empty((chunk, m2, m1, s, s, s), dtype=src.tensor.dtype, device=device)
             if stats is not None:
                 stats.allocate("coeff_field", coeff.numel() * coeff.element_size())
             try:
@@ -380,6 +394,7 @@ def run_steps(
     dt: float | None = None,
     first_step: int = 0,
     stats: AllocationStats | None = None,
+    graph: bool | None = None,
 ) -> None:
     """`steps` full steps with ONE host synchronisation at the end.
 
@@ -387,6 +402,9 @@ def run_steps(
     after an instability nothing further is computed, and the error raised
     names the same half step and node the per-step loop of the reference
     (runner.py:160-168) would have reported.
+
+    graph: replay the steps from a captured CUDA graph (fused mode; removes the per-launch
+    host cost that dominates small grids).  None = automatic: fused grids up to 64^3 cells.
     """
     if state.grid.parity != "primary" or scratch.grid.parity != "dual":
         raise ValueError("run_steps expects state on the primary grid and scratch on the dual grid")
@@ -394,6 +412,13 @@ def run_steps(
         return
     if dt is None:
         dt = select_dt(state.grid, cfg)
+    if graph is None:
+        graph = cfg.mode == "fused" and state.grid.num_cells <= 64 ** 3 and steps >= 8
+    if graph:
+        if cfg.mode != "fused":
+            raise ValueError("graph replay is available for the fused mode")
+        _run_steps_graph(state, scratch, cfg, ops, steps, dt, first_step)
+        return
     flags = _new_flags(2 * steps, state.device)
     prev = None
     for k in range(steps):
@@ -406,3 +431,42 @@ def run_steps(
     host = flags.cpu().numpy()
     _raise_first_bad(host, (scratch.grid, state.grid),
                      [first_step + k // 2 for k in range(2 * steps)])
+
+
+# captured step blocks, keyed by (fields, config, dt, block length); a graph replays its kernels
+# with the field pointers baked in, so it is only reused for the same state/scratch tensors
+_GRAPHS: dict = {}
+
+
+def _run_steps_graph(state, scratch, cfg, ops, steps, dt, first_step, block: int = 32) -> None:
+    """Replay blocks of `block` full steps from a CUDA graph; the flags are read back once per
+    replay (the guard chain inside a block skips everything after an instability)."""
+    dev = state.device
+    cur = torch.cuda.current_stream(dev)
+    done = 0
+    while done < steps:
+        nb = min(block, steps - done)
+        key = (state.tensor.data_ptr(), scratch.tensor.data_ptr(), tuple(state.tensor.shape), cfg, ops.order_n,
+               float(dt), nb, dev.index)
+        entry = _GRAPHS.get(key)
+        if entry is None:
+            flags = _new_flags(2 * nb, dev)
+            g = torch.cuda.CUDAGraph()
+            side = torch.cuda.Stream(dev)
+            side.wait_stream(cur)
+            with torch.cuda.graph(g, stream=side):
+                flags.fill_(-1)
+                prev = None
+                for k in range(nb):
+                    f0, f1 = flags[2 * k:2 * k + 1], flags[2 * k + 1:2 * k + 2]
+                    half_step(state, scratch, cfg, ops, dt=dt, _flag=f0, _guard=prev, _check=False)
+                    half_step(scratch, state, cfg, ops, dt=dt, _flag=f1, _guard=f0, _check=False)
+                    prev = f1
+            cur.wait_stream(side)
+            entry = _GRAPHS[key] = (g, flags, state.tensor, scratch.tensor)
+        g, flags = entry[0], entry[1]
+        g.replay()
+        host = flags.cpu().numpy()
+        _raise_first_bad(host, (scratch.grid, state.grid),
+                         [first_step + done + k // 2 for k in range(2 * nb)])
+        done += nb

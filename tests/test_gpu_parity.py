@@ -423,3 +423,32 @@ def test_constant_operator_ring_cross_stream_upload_order():
         torch.cuda.synchronize()
         for o in outs:
             assert rm.rel_err(o.cpu().numpy(), ref.cpu().numpy()) <= 1e-13
+
+
+@pytest.mark.parametrize("order_n,cells,steps", [(3, (12, 10, 9), 37), (5, (8, 8, 6), 9), (1, (16, 16, 16), 40)])
+def test_run_steps_graph_replay_bitwise(order_n, cells, steps):
+    """CUDA-graph replay of run_steps equals the eager launches bit for bit (several blocks and a
+    partial last block), and a graph is reused across calls."""
+    grid = hb.GridSpec(cells)
+    cfg = hb.StepConfig(variant="separable")
+    ops = hb.OperatorSet.for_grid(grid, order_n)
+    outs = []
+    for graph in (False, True):
+        st = hb.init_field(hb.plane_wave(), grid, order_n)
+        sc = hb.DofField.zeros(grid.with_parity("dual"), order_n)
+        hb.run_steps(st, sc, cfg, ops, steps, graph=graph)
+        hb.run_steps(st, sc, cfg, ops, steps, graph=graph)
+        outs.append(st.tensor.clone())
+    assert torch.equal(outs[0], outs[1])
+
+
+def test_run_steps_graph_reports_instability_step():
+    grid = hb.GridSpec((8, 7, 6))
+    cfg = hb.StepConfig(variant="separable")
+    ops = hb.OperatorSet.for_grid(grid, 3)
+    st = hb.init_field(hb.plane_wave(), grid, 3)
+    sc = hb.DofField.zeros(grid.with_parity("dual"), 3)
+    st.tensor[3, 2, 1, 0, 0, 0] = float("nan")
+    with pytest.raises(hb.InstabilityError) as err:
+        hb.run_steps(st, sc, cfg, ops, 20, first_step=5, graph=True)
+    assert err.value.step == 5
