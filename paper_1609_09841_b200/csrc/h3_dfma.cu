@@ -32,7 +32,7 @@ template <> struct RcTile<0> { static constexpr int TX = 16, TY = 8, THREADS = 2
 template <> struct RcTile<1> { static constexpr int TX = 8, TY = 8, THREADS = 256, MINB = 2; };
 template <> struct RcTile<2> { static constexpr int TX = 8, TY = 4, THREADS = 384, MINB = 1; };
 template <> struct RcTile<3> { static constexpr int TX = 8, TY = 4, THREADS = 512, MINB = 1; };
-template <> struct RcTile<4> { static constexpr int TX = 4, TY = 4, THREADS = 320, MINB = 1; };
+template <> struct RcTile<4> { static constexpr int TX = 4, TY = 2, THREADS = 800, MINB = 1; };
 template <> struct RcTile<5> { static constexpr int TX = 4, TY = 2, THREADS = 384, MINB = 1; };
 
 template <int N>
