@@ -64,8 +64,11 @@ using tma::mbar_wait;
 // ABL (measurement-only ablations, results are garbage): bit 0 skips the global stores,
 // bit 1 the input copies, bit 2 replaces every DMMA by a register update.
 template <int TY_, int WARPS_, int STAGES_, bool VALIAS_, int MINB_ = 1, int ABL_ = 0, bool TMA_ = false,
-          bool LEAN_ = false, int PIPE_ = 0>
+          bool LEAN_ = false, int PIPE_ = 0, bool CF_ = false>
 struct Dm3Cfg {
+    // CF: W cell stride 84 and an odd V row stride, so the paired stores of x1 / x2 (the two lane
+    // halves write neighbouring cells / cell rows) hit distinct banks (80 and 8 x 68 are 0 mod 16)
+    static constexpr bool CF = CF_;
     // PIPE 1: x3 of plane p-1 shares a barrier interval with x1 of plane p (2 barriers/plane).
     // (A 1-barrier variant -- x3(p-2), x2(p-1), x1(p) with W and V doubled -- measured 17 % slower.)
     static constexpr int PIPE = PIPE_;
@@ -81,15 +84,16 @@ struct Dm3Cfg {
     static constexpr int WARPS = WARPS_, THREADS = 32 * WARPS, STAGES = STAGES_;
     static constexpr bool VALIAS = VALIAS_;  // x2 output reuses the consumed input stage
     static constexpr int UNS = 64;            // U node stride (dense [j3][j2][j1])
-    static constexpr int WRS = 20, WCS = 80;  // W  [j3][m1][j2]: j3-row stride, cell stride
+    static constexpr int WRS = 20, WCS = CF ? 84 : 80;  // W  [j3][m1][j2]: j3-row stride, cell stride
     static constexpr int VRS = 17, VCS = 68;  // V  [m2][m1][j3]: m2-row stride, cell stride
+    static constexpr int VROW = TX * VCS + (CF ? 1 : 0);  // V cell-row stride
     static constexpr int T1 = 2 * NY, K1 = (T1 + WARPS - 1) / WARPS;  // x1 (row, half) tasks
     static constexpr int T2 = 2 * TX, K2 = (T2 + WARPS - 1) / WARPS;  // x2 (column, half) tasks
     static constexpr int T3 = 2 * TX * TY, K3 = T3 / WARPS;           // x3 (cell, half) chains
     static constexpr int CPW = (NCOL + WARPS - 1) / WARPS;            // node copies per warp
     static constexpr size_t U_D = (size_t)NCOL * UNS;
     static constexpr size_t W_D = (size_t)NY * TX * WCS;
-    static constexpr size_t V_D = (size_t)TY * TX * VCS;
+    static constexpr size_t V_D = (size_t)TY * VROW;
     static constexpr size_t SMEM_DATA =
         (STAGES * U_D + W_D + (VALIAS ? 0 : V_D)) * sizeof(double);
     static constexpr size_t SMEM = SMEM_DATA + (TMA ? STAGES * sizeof(uint64_t) : 0);
@@ -106,7 +110,7 @@ sep_fused_dmma3_kernel(const double* __restrict__ src, double* __restrict__ dst,
                        unsigned long long* first_bad, const unsigned long long* guard) {
     constexpr int n = C::n, n3 = C::n3, TX = C::TX, TY = C::TY, NX = C::NX, NY = C::NY;
     constexpr int NCOL = C::NCOL, WARPS = C::WARPS, STAGES = C::STAGES, UNS = C::UNS;
-    constexpr int WRS = C::WRS, WCS = C::WCS, VRS = C::VRS, VCS = C::VCS;
+    constexpr int WRS = C::WRS, WCS = C::WCS, VRS = C::VRS, VCS = C::VCS, VROW = C::VROW;
     constexpr int K1 = C::K1, K2 = C::K2, K3 = C::K3;
     if (guarded_out(guard, first_bad)) return;
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -316,7 +320,7 @@ sep_fused_dmma3_kernel(const double* __restrict__ src, double* __restrict__ dst,
                     if (ly & 1) {
                         if (ly == NY - 1) {  // lone last cell row: half-warp store
                             if (done && live[j]) {
-                                double* v = vcol[j] + (ly - 1) * TX * VCS;
+                                double* v = vcol[j] + (ly - 1) * VROW;
                                 v[0] = r[j][0];
                                 v[VRS] = r[j][1];
                             }
@@ -325,7 +329,7 @@ sep_fused_dmma3_kernel(const double* __restrict__ src, double* __restrict__ dst,
                             sv[j][1] = r[j][1];
                         }
                     } else if (ly > 0 && live[j]) {
-                        double* v = vcol[j] + (ly - 1 - (par ^ 1)) * TX * VCS;
+                        double* v = vcol[j] + (ly - 1 - (par ^ 1)) * VROW;
                         v[0] = par ? r[j][0] : sv[j][0];
                         v[VRS] = par ? r[j][1] : sv[j][1];
                     }
@@ -347,7 +351,7 @@ sep_fused_dmma3_kernel(const double* __restrict__ src, double* __restrict__ dst,
                 const int t = warp + WARPS * k;
                 const int cell = t >> 1, h = t & 1;
                 const int L = 8 * h + g;  // line (m2, m1) = (L >> 2, L & 3)
-                const double a = V[cell * VCS + (L >> 2) * VRS + (L & 3) * 4 + q];
+                const double a = V[(cell / TX) * VROW + (cell % TX) * VCS + (L >> 2) * VRS + (L & 3) * 4 + q];
                 const int ph = (pp + k) & 1;
                 dmma_abl<C::ABL>(acc[k][0], acc[k][1], a, ph ? bop[2][1] : bop[2][0]);
                 const bool done = par == ((pp + k + 1) & 1);
@@ -507,8 +511,10 @@ int sep_fused_dmma3_launch(const double* src, double* dst, const Dims& d, const 
         case 14: return launch_dm3<Dm3Cfg<7, 16, 3, true, 1, 4, true>>(src, dst, d, ops, off, st, first_bad, guard);
         case 15: return launch_dm3<Dm3Cfg<7, 16, 3, true, 1, 5, true>>(src, dst, d, ops, off, st, first_bad, guard);
         case 16: return launch_dm3<Dm3Cfg<7, 16, 3, true, 1, 0, true>>(src, dst, d, ops, off, st, first_bad, guard);
-        // default: TMA row loads, x3(p-1) pipelined with x1(p) (2 barriers per plane), lean x3 stores
-        default: return launch_dm3<Dm3Cfg<7, 16, 3, false, 1, 0, true, true, 1>>(src, dst, d, ops, off, st, first_bad, guard);
+        case 31: return launch_dm3<Dm3Cfg<7, 16, 3, false, 1, 0, true, true, 1, false>>(src, dst, d, ops, off, st, first_bad, guard);  // bank-conflicted W/V
+        // default: TMA row loads, x3(p-1) pipelined with x1(p) (2 barriers per plane), lean x3 stores,
+        // conflict-free W / V strides
+        default: return launch_dm3<Dm3Cfg<7, 16, 3, false, 1, 0, true, true, 1, true>>(src, dst, d, ops, off, st, first_bad, guard);
     }
 }
 
