@@ -319,8 +319,13 @@ sep_evolve_kernel(const double* __restrict__ coeff, double* __restrict__ dst, Di
                   const unsigned long long* guard) {
     constexpr int n = N + 1, S = 2 * n, S2 = S * S, S3 = S2 * S, n2 = n * n, n3 = n2 * n;
     constexpr int THREADS = CPB * S2;
-    constexpr int T1S = S2 * n + 1;  // per-cell stride of the pass-x1 output (odd: spreads banks)
-    constexpr int T2S = S * n2 + 1;
+    // shared layouts T1[c][i3][i2][m1] = c T1S + i3 A3 + i2 A2 + m1 and T2[c][i3][m2][m1] =
+    // c T2S + i3 B3 + m2 B2 + m1; at N = 3 the strides come from tools/evolve_layout_search.py
+    // (64 instead of 168 shared wavefronts per cell: every x1 store and x3 load conflict-free)
+    constexpr int A2 = N == 3 ? 5 : n, A3 = N == 3 ? 40 : S * n;
+    constexpr int B2 = n, B3 = N == 3 ? 20 : n2;
+    constexpr int T1S = S * A3 + 1;  // per-cell strides (odd: spreads banks across cells)
+    constexpr int T2S = S * B3 + 1;
     __shared__ double T1[CPB * T1S];  // [c][i3][i2][m1]
     __shared__ double T2[CPB * T2S];  // [c][i3][m2][m1]
 
@@ -362,7 +367,7 @@ sep_evolve_kernel(const double* __restrict__ coeff, double* __restrict__ dst, Di
             double acc = p.Sh[0][m][0] * u[gi][0];
 #pragma unroll
             for (int k = 1; k < S; ++k) acc = fma(p.Sh[0][m][k], u[gi][k], acc);
-            T1[c * T1S + line * n + m] = acc;
+            T1[c * T1S + (line / S) * A3 + (line % S) * A2 + m] = acc;
         }
         __syncthreads();
         // pass x2: (c, i3, m1) -> n outputs m2
@@ -370,13 +375,13 @@ sep_evolve_kernel(const double* __restrict__ coeff, double* __restrict__ dst, Di
             const int cc = l / (S * n), r = l - cc * (S * n), i3 = r / n, mm1 = r - (r / n) * n;
             double a[S];
 #pragma unroll
-            for (int k = 0; k < S; ++k) a[k] = T1[cc * T1S + (i3 * S + k) * n + mm1];
+            for (int k = 0; k < S; ++k) a[k] = T1[cc * T1S + i3 * A3 + k * A2 + mm1];
 #pragma unroll
             for (int m = 0; m < n; ++m) {
                 double acc = p.Sh[1][m][0] * a[0];
 #pragma unroll
                 for (int k = 1; k < S; ++k) acc = fma(p.Sh[1][m][k], a[k], acc);
-                T2[cc * T2S + (i3 * n + m) * n + mm1] = acc;
+                T2[cc * T2S + i3 * B3 + m * B2 + mm1] = acc;
             }
         }
         __syncthreads();
@@ -387,7 +392,7 @@ sep_evolve_kernel(const double* __restrict__ coeff, double* __restrict__ dst, Di
             if (cell >= total) continue;
             double a[S];
 #pragma unroll
-            for (int k = 0; k < S; ++k) a[k] = T2[cc * T2S + k * n2 + r];
+            for (int k = 0; k < S; ++k) a[k] = T2[cc * T2S + k * B3 + r];
             const int64_t crel3 = cell / nxy, rem = cell - crel3 * nxy;
             const int64_t node = ((d.z_begin + crel3) * d.M2 + rem / d.M1) * d.M1 + rem % d.M1;
             double* o = dst + node * n3 + r;
