@@ -3,8 +3,11 @@ wavefronts of the x1 stores, x2 loads/stores and x3 loads (8-byte accesses: a wa
 as two 16-lane half-warps; 16 double-wide banks; distinct doubles in one bank serialise)."""
 import itertools
 
-N = 3
+import sys
+
+N = int(sys.argv[1]) if len(sys.argv) > 1 else 3
 n, S = N + 1, 2 * N + 2
+CPB = max(1, 256 // (S * S)) if N != 3 else 1
 
 
 def wavefronts(addrs):
