@@ -327,7 +327,11 @@ def main():
         del scratch
         scratch = None
         torch.cuda.empty_cache()
-        result["e2e"] = e2e_host(hb, torch, state, grid, order_n, cfg, dt, args.e2e_steps, dofs_per_step)
+        try:
+            result["e2e"] = e2e_host(hb, torch, state, grid, order_n, cfg, dt, args.e2e_steps, dofs_per_step)
+        except (RuntimeError, MemoryError) as exc:  # e.g. not enough host RAM for the field
+            result["e2e"] = {"value": None, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0,
+                             "error": f"{type(exc).__name__}: {exc}"[:300]}
         print(f"[bench] e2e {result['e2e']}", file=sys.stderr, flush=True)
     # ---- CPU baseline (rank 0, N = 1) ----------------------------------------------------------
     if world == 1 and not args.no_cpu:
