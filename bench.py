@@ -55,6 +55,9 @@ def parse():
     ap.add_argument("--no-extras", action="store_true",
                     help="skip the secondary configs (two-kernel 512^3 / 128^3, m=5 256^3)")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    ap.add_argument("--halo", default="auto", choices=["auto", "nccl", "p2p"],
+                    help="N>1 halo: in-kernel reads of the neighbour plane over NVLink (p2p), NCCL copy, "
+                         "or auto (p2p verified against NCCL at start-up, else NCCL)")
     ap.add_argument("--backend", default="nccl", choices=["nccl", "gloo"],
                     help="process-group backend for N>1 (gloo: test the multi-rank path on one GPU)")
     return ap.parse_args()
@@ -231,7 +234,7 @@ def main():
 
     if world > 1:
         solver = hd.SlabSolver((m, m, m * world), order_n, hb.StepConfig(mode=args.mode, variant=args.variant),
-                               lengths=(1.0, 1.0, float(world)))
+                               lengths=(1.0, 1.0, float(world)), halo=args.halo)
         solver.init(hb.plane_wave())
         step_fn = solver.step
         launches_per_step = solver.launches_per_step
@@ -306,6 +309,7 @@ def main():
                                f"({args.variant}) half-step kernels, periodic advection, cfl 0.9, q={3 * (2 * order_n + 1)}",
                    "order_m": order_n, "cells_per_gpu": [m, m, m], "global_cells": [m, m, m * world],
                    "mode": args.mode, "variant": args.variant, "parallelism": f"slab-x3 x{world}",
+                   "halo": (solver.halo + (f" ({solver.halo_note})" if solver.halo_note else "")) if world > 1 else None,
                    "l2": f"inputs larger than L2 ({dofs_per_step // world * 8 / 1e9:.1f} GB per field vs 126 MB L2)"},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak_gbs, "unit": "GB/s",
                      "frac": (achieved / peak_gbs) if achieved else None, "traffic": traffic,

@@ -72,6 +72,25 @@ int h3_fused_pass_f32(const float* src, float* dst, int64_t M1, int64_t M2, int6
                       int64_t z_end, int periodic_z, int variant, void* stream,
                       unsigned long long* d_first_bad, const unsigned long long* d_guard);
 
+/* Fused half step of an x3 slab [z_begin, z_end) of an M3-plane field whose ghost planes -1 and M3
+ * are NOT stored next to it: ghost_lo / ghost_hi point at those planes wherever they live -- in
+ * the multi-GPU solver, the neighbour rank's boundary plane mapped through CUDA IPC, read in
+ * place over NVLink by the kernel's TMA plane loads (no separate halo copy).  Separable variant,
+ * N = 3 and 5 (H3_ERR_VARIANT otherwise).  Synchronising the neighbours (the plane must be final
+ * before it is read and not rewritten while it is read) is the caller's job. */
+int h3_fused_pass_halo(const double* src, double* dst, int64_t M1, int64_t M2, int64_t M3,
+                       int order_n, const double* h_mat, const double* fac1, const double* fac2,
+                       const double* fac3, const double* cfac, int q, int off, int64_t z_begin,
+                       int64_t z_end, const double* ghost_lo, const double* ghost_hi, int variant,
+                       void* stream, unsigned long long* d_first_bad,
+                       const unsigned long long* d_guard);
+
+/* CUDA IPC helpers for the halo mapping: export the 64-byte handle of the allocation containing
+ * `ptr` and ptr's byte offset in it; open / close a peer allocation. */
+int h3_ipc_export(const void* ptr, unsigned char* handle64, int64_t* offset);
+int h3_ipc_open(const unsigned char* handle64, void** base_out);
+int h3_ipc_close(void* base);
+
 /* Replaces gridkernels.recon_pass(src, coeff, h_mat, tiles, off) (gridkernels.py:142-160;
  * pipeline.py:262).  coeff holds only the cells [z_begin, z_end) (slab chunk):
  * coeff[(c3 - z_begin)][c2][c1][s][s][s].  variant LITERAL = reference summation

@@ -38,6 +38,11 @@ SIGNATURES = {
     "h3_error_norms": (_i32, [_vp, _i64, _i64, _i64, _i32, _i32, _vp, _vp, _vp, _vp, _i64, _vp,
                               _vp]),
     "h3_check_finite": (_i32, [_vp, _i64, _i64, _i64, _i32, _u64p, _vp]),
+    "h3_fused_pass_halo": (_i32, [_vp, _vp, _i64, _i64, _i64, _i32, _vp, _vp, _vp, _vp, _vp, _i32, _i32,
+                                  _i64, _i64, _vp, _vp, _i32, _vp, _u64p, _u64p]),
+    "h3_ipc_export": (_i32, [_vp, _vp, _vp]),
+    "h3_ipc_open": (_i32, [_vp, _vp]),
+    "h3_ipc_close": (_i32, [_vp]),
     "h3_version": (ctypes.c_char_p, []),
     "h3_error_string": (ctypes.c_char_p, [_i32]),
     "h3_max_order": (_i32, []),

@@ -174,7 +174,81 @@ static int evolve_impl(const T* coeff, T* dst, int64_t M1, int64_t M2, int64_t M
                                  q, 0, st, d_first_bad, d_guard);
 }
 
+// Fused half step of a slab whose ghost planes are held elsewhere (peer GPU memory).
+static int fused_halo_impl(const double* src, double* dst, int64_t M1, int64_t M2, int64_t M3, int order_n,
+                           const double* h_mat, const double* fac1, const double* fac2, const double* fac3,
+                           const double* cfac, int q, int off, int64_t z_begin, int64_t z_end,
+                           const double* ghost_lo, const double* ghost_hi, int variant, void* stream,
+                           unsigned long long* d_first_bad, const unsigned long long* d_guard) {
+    int rc = check_common(M1, M2, M3, order_n, z_begin, z_end);
+    if (rc) return rc;
+    if (!src || !dst || !h_mat || !fac1 || !fac2 || !fac3 || !cfac) return H3_ERR_ARG;
+    if (off != 0 && off != -1) return H3_ERR_ARG;
+    if (off == 0 && z_end == M3 && !ghost_hi) return H3_ERR_ARG;   // cell M3-1 reads plane M3
+    if (off == -1 && z_begin == 0 && !ghost_lo) return H3_ERR_ARG;  // cell 0 reads plane -1
+    if (q < 1 || q > H3_MAX_STAGES) return H3_ERR_STAGES;
+    if (q < exact_stages(order_n)) return H3_ERR_STAGES;
+    // the tile-march kernels with TMA plane loads take the ghost pointers (N = 3, 5)
+    if ((variant != H3_VARIANT_AUTO && variant != H3_VARIANT_SEPARABLE) || (order_n != 3 && order_n != 5))
+        return H3_ERR_VARIANT;
+    Dims d{M1, M2, M3, z_begin, z_end, 0};
+    d.ghost_lo = ghost_lo;
+    d.ghost_hi = ghost_hi;
+    const int n = order_n + 1, s = 2 * n;
+    double A[3 * (H3_MAX_ORDER + 1) * (2 * H3_MAX_ORDER + 2)];
+    h3::build_separable(order_n, h_mat, fac1, fac2, fac3, cfac[0], A, nullptr);
+    (void)s;
+    (void)n;
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    return order_n == 3 ? h3::sep_fused_dmma3_launch(src, dst, d, A, off, st, d_first_bad, d_guard)
+                        : h3::sep_fused_dmma5_launch(src, dst, d, A, off, st, d_first_bad, d_guard);
+}
+
 extern "C" {
+
+int h3_fused_pass_halo(const double* src, double* dst, int64_t M1, int64_t M2, int64_t M3, int order_n,
+                       const double* h_mat, const double* fac1, const double* fac2, const double* fac3,
+                       const double* cfac, int q, int off, int64_t z_begin, int64_t z_end,
+                       const double* ghost_lo, const double* ghost_hi, int variant, void* stream,
+                       unsigned long long* d_first_bad, const unsigned long long* d_guard) {
+    return fused_halo_impl(src, dst, M1, M2, M3, order_n, h_mat, fac1, fac2, fac3, cfac, q, off, z_begin,
+                           z_end, ghost_lo, ghost_hi, variant, stream, d_first_bad, d_guard);
+}
+
+// CUDA IPC of a device buffer that may sit inside a larger allocation (torch's caching
+// allocator): export the handle of the containing allocation plus the byte offset.
+typedef int (*h3_cuMemGetAddressRange_t)(unsigned long long*, size_t*, unsigned long long);
+
+int h3_ipc_export(const void* ptr, unsigned char* handle64, int64_t* offset) {
+    if (!ptr || !handle64 || !offset) return H3_ERR_ARG;
+    static h3_cuMemGetAddressRange_t range = [] {
+        void* fn = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuMemGetAddressRange", &fn, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess)
+            return (h3_cuMemGetAddressRange_t) nullptr;
+        return (h3_cuMemGetAddressRange_t)fn;
+    }();
+    if (!range) return (int)cudaErrorNotSupported;
+    unsigned long long base = 0;
+    size_t size = 0;
+    if (range(&base, &size, (unsigned long long)(uintptr_t)ptr) != 0) return (int)cudaErrorInvalidDevicePointer;
+    cudaIpcMemHandle_t h;
+    cudaError_t e = cudaIpcGetMemHandle(&h, (void*)(uintptr_t)base);
+    if (e != cudaSuccess) return (int)e;
+    memcpy(handle64, &h, sizeof(h));
+    *offset = (int64_t)((uintptr_t)ptr - (uintptr_t)base);
+    return 0;
+}
+
+int h3_ipc_open(const unsigned char* handle64, void** base_out) {
+    if (!handle64 || !base_out) return H3_ERR_ARG;
+    cudaIpcMemHandle_t h;
+    memcpy(&h, handle64, sizeof(h));
+    return (int)cudaIpcOpenMemHandle(base_out, h, cudaIpcMemLazyEnablePeerAccess);
+}
+
+int h3_ipc_close(void* base) { return base ? (int)cudaIpcCloseMemHandle(base) : H3_ERR_ARG; }
 
 int h3_fused_pass(const double* src, double* dst, int64_t M1, int64_t M2, int64_t M3, int order_n,
                   const double* h_mat, const double* fac1, const double* fac2, const double* fac3,

@@ -116,7 +116,7 @@ recon_sep_kernel(const double* __restrict__ src, double* __restrict__ coeff, Dim
     int issued = 0;
     auto issue = [&]() {
         if (issued < P) {
-            const double* base = src + gz_next * plane_elems;
+            const double* base = plane_base(src, gz_next, plane_elems, d);
             double* Ub = U + (issued % STAGES) * G::U_D;
             constexpr int PER = G::V16 ? 2 : 1, PPN = n3 / PER;  // pieces per node
 #pragma unroll 1

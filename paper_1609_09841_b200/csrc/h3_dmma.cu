@@ -180,7 +180,7 @@ sep_fused_dmma3_kernel(const double* __restrict__ src, double* __restrict__ dst,
                     fence_proxy_async_smem();
                     if (warp == 0) mbar_arrive_expect_tx(&bars[s], (unsigned)(NCOL * UNS * sizeof(double)));
                     if (!(C::ABL & 2)) {
-                        const double* base = src + gz_next * plane_elems + (int64_t)rowoff * n3;
+                        const double* base = plane_base(src, gz_next, plane_elems, d) + (int64_t)rowoff * n3;
                         double* Ub = U + s * C::U_D + warp * NX * UNS;
                         int got = 0, gx = gx0;
                         while (got < NX) {
@@ -198,7 +198,7 @@ sep_fused_dmma3_kernel(const double* __restrict__ src, double* __restrict__ dst,
             }
         } else {
             if (issued < P) {
-                const double* base = src + gz_next * plane_elems;
+                const double* base = plane_base(src, gz_next, plane_elems, d);
                 double* Ub = U + (issued % STAGES) * C::U_D + 2 * lane;
 #pragma unroll
                 for (int j = 0; j < C::CPW; ++j)
@@ -588,7 +588,7 @@ recon_dmma3_kernel(const double* __restrict__ src, double* __restrict__ coeff, D
     int issued = 0;
     auto issue = [&]() {
         if (issued < P) {
-            const double* base = src + gz_next * plane_elems;
+            const double* base = plane_base(src, gz_next, plane_elems, d);
             double* Ub = U + (issued % STAGES) * U_D + 2 * lane;
 #pragma unroll
             for (int j = 0; j < CPW; ++j)

@@ -116,7 +116,7 @@ sep_fused_dmma_cp_kernel(const double* __restrict__ src, double* __restrict__ ds
                 const int s = issued % STAGES;
                 fence_proxy_async_smem();
                 if (warp == 0) mbar_arrive_expect_tx(&bars[s], (unsigned)(C::NNODE * UNS * sizeof(double)));
-                const double* base = src + gz_next * plane_elems + (int64_t)rowoff * n3;
+                const double* base = plane_base(src, gz_next, plane_elems, d) + (int64_t)rowoff * n3;
                 double* Ub = U + s * C::U_D + warp * NX * UNS;
                 int got = 0, gx = gx0;
                 while (got < NX) {
@@ -373,7 +373,7 @@ recon_dmma_cp_kernel(const double* __restrict__ src, double* __restrict__ coeff,
                 const int s = issued % STAGES;
                 fence_proxy_async_smem();
                 if (warp == 0) mbar_arrive_expect_tx(&bars[s], (unsigned)(C::NNODE * UNS * sizeof(double)));
-                const double* base = src + gz_next * plane_elems + (int64_t)rowoff * n3;
+                const double* base = plane_base(src, gz_next, plane_elems, d) + (int64_t)rowoff * n3;
                 double* Ub = U + s * C::U_D + warp * NX * UNS;
                 int got = 0, gx = gx0;
                 while (got < NX) {

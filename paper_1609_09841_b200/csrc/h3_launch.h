@@ -16,7 +16,20 @@ struct Dims {
     int64_t M1, M2, M3;
     int64_t z_begin, z_end;
     int periodic_z;
+    // periodic_z == 0 only: where the ghost planes -1 and M3 live when they are not stored next
+    // to the field (h3_fused_pass_halo: the neighbour's boundary plane, read in place over
+    // NVLink through a CUDA-IPC mapping); nullptr = contiguous with the field
+    const double* ghost_lo = nullptr;
+    const double* ghost_hi = nullptr;
 };
+
+// Base of node plane gz of a (slab) field: the field itself, or a separately held ghost plane.
+__device__ __forceinline__ const double* plane_base(const double* src, int64_t gz, int64_t plane_elems,
+                                                    const Dims& d) {
+    if (d.ghost_lo != nullptr && gz < 0) return d.ghost_lo;
+    if (d.ghost_hi != nullptr && gz >= d.M3) return d.ghost_hi;
+    return src + gz * plane_elems;
+}
 
 // Literal (bit-faithful) operator bundle: exactly the reference's factor arrays
 // (pipeline.py:197-207), carried as kernel parameters (constant bank).

@@ -13,11 +13,18 @@ the gather offset (reference gridkernels.py:46, g = c + off + a):
              local plane of rank+1 (send my first plane to rank-1);
     off = -1 (dual -> primary): cell c needs nodes c-1, c  -> ghost_lo = last
              local plane of rank-1 (send my last plane to rank+1).
-The ranks form a periodic ring.  On the GPU the exchange is an NCCL
-send/recv pair (over NVLink/NVSwitch) issued before the interior cell planes
-are launched, so it overlaps with them; the one boundary cell plane that
-reads the ghost is launched after the exchange completes.  The kernels read
-the ghost planes directly (h3_fused_pass with periodic_z = 0).
+The ranks form a periodic ring.  Two halo implementations:
+
+* "nccl" (default): an NCCL send/recv pair (over NVLink/NVSwitch) copies the
+  neighbour's plane into the ghost plane; it is issued before the interior
+  cell planes are launched, so it overlaps with them, and the one boundary
+  cell plane that reads the ghost is launched after the exchange completes
+  (h3_fused_pass with periodic_z = 0).
+* "p2p": no copy at all -- the neighbours' field buffers are mapped through
+  CUDA IPC once, and the kernel's TMA plane loads read the neighbour's
+  boundary plane in place over NVLink (h3_fused_pass_halo); a stream-ordered
+  all-reduce of one element per half step is the only collective (it orders
+  the neighbours' previous half step before the read and the overwrite).
 """
 
 from __future__ import annotations
@@ -94,7 +101,8 @@ class SlabSolver:
     return views of the local planes.  Used by bench.py for the 2/4/8-GPU runs.
     """
 
-    def __init__(self, global_cells, order_n: int, cfg: StepConfig, lengths=(1.0, 1.0, 1.0), group=None):
+    def __init__(self, global_cells, order_n: int, cfg: StepConfig, lengths=(1.0, 1.0, 1.0), group=None,
+                 halo: str = "nccl"):
         self.group = group
         self.world = dist.get_world_size(group) if dist.is_initialized() else 1
         self.rank = dist.get_rank(group) if dist.is_initialized() else 0
@@ -113,12 +121,33 @@ class SlabSolver:
         self.dt = select_dt(self.grid, cfg)
         self.flags = torch.full((2,), -1, dtype=torch.int64, device="cuda")
         self.kernel_events = []
-        self.launches_per_step = 4
         q = cfg.stages(order_n)
         self._fac = _factor_arrays(self.ops, np.float64, self.dt / 2, q)
         self._q = q
         if cfg.mode != "fused":
             raise NotImplementedError("SlabSolver runs the fused half step")
+        if halo not in ("nccl", "p2p", "auto"):
+            raise ValueError(f"halo must be 'nccl', 'p2p' or 'auto', got {halo!r}")
+        self.halo = halo
+        self.halo_note = ""
+        if halo == "auto":
+            # in-kernel p2p halo where it is available (N = 3, 5), verified against the NCCL copy
+            # on the first initialised field (init); any failure falls back to NCCL
+            if order_n in (3, 5):
+                try:
+                    self._setup_p2p()
+                except Exception as exc:  # noqa: BLE001 -- any mapping failure means "use NCCL"
+                    self.halo, self.halo_note = "nccl", f"p2p setup failed: {exc}"
+            else:
+                self.halo, self.halo_note = "nccl", "p2p halo kernels exist for N = 3, 5"
+        elif halo == "p2p":
+            self._setup_p2p()
+
+    @property
+    def launches_per_step(self) -> int:
+        """Kernel launches per full step: one per half step with the in-kernel halo, two (interior
+        + boundary plane) with the NCCL copy."""
+        return 2 if self.halo == "p2p" else 4
 
     @property
     def state(self) -> torch.Tensor:
@@ -135,6 +164,32 @@ class SlabSolver:
         m1, m2, _ = self.grid.cells_per_axis
         launch_init(self.state, (m1, m2, self.local), self.order_n,
                     (t1, t2, np.ascontiguousarray(t3[:, self.z0:self.z1])))
+        if self.halo == "auto":
+            self._verify_p2p()
+
+    def _verify_p2p(self) -> None:
+        """One half step through both halo paths from the current state; all ranks must agree
+        bit for bit, else the solver uses the NCCL copy from now on."""
+        ok = True
+        try:
+            saved = self.bufs[1].clone()
+            flag = torch.full((1,), -1, dtype=torch.int64, device="cuda")
+            self._half_p2p(0, 1, 0, flag, False)
+            via_p2p = self.bufs[1][1:-1].clone()
+            self.half_step(self.bufs[0], self.bufs[1], 0, flag)
+            ok = bool(torch.equal(via_p2p, self.bufs[1][1:-1]))
+            self.bufs[1].copy_(saved)
+        except Exception as exc:  # noqa: BLE001
+            ok, self.halo_note = False, f"p2p verification raised: {exc}"
+        votes = torch.tensor([0.0 if ok else 1.0], device="cuda" if self.world == 1 or
+                             dist.get_backend(self.group) == "nccl" else "cpu")
+        if self.world > 1:
+            dist.all_reduce(votes, group=self.group)
+        if float(votes.item()) == 0.0:
+            self.halo = "p2p"
+        else:
+            self.halo = "nccl"
+            self.halo_note = self.halo_note or "p2p result differed from the NCCL halo"
 
     def _launch(self, src, dst, off, zb, ze, flag, events):
         m1, m2, _ = self.grid.cells_per_axis
@@ -155,6 +210,85 @@ class SlabSolver:
             e1.record(stream)
             events.append((e0, e1))
 
+    # ---- p2p halo: the kernel reads the neighbour's boundary plane in place (CUDA IPC / NVLink) ----
+    def _setup_p2p(self):
+        """Map the neighbours' field buffers (CUDA IPC handles exchanged through the process
+        group); with one rank the 'neighbours' are the rank itself (periodic wrap)."""
+        if self.order_n not in (3, 5):
+            raise NotImplementedError("the in-kernel p2p halo is implemented for N = 3 and 5")
+        lib = _native.lib()
+        mine = []
+        for b in self.bufs:
+            h = (ctypes.c_ubyte * 64)()
+            off = ctypes.c_int64()
+            _native.check(lib.h3_ipc_export(ctypes.c_void_p(b.data_ptr()), h, ctypes.byref(off)), "h3_ipc_export")
+            mine.append((bytes(h), int(off.value), self.local))
+        everyone = [None] * self.world
+        if self.world > 1:
+            dist.all_gather_object(everyone, mine, group=self.group)
+        else:
+            everyone = [mine]
+        self._opened = []
+        self._peer = {}  # rank -> ([buf0 ptr, buf1 ptr], local planes); ptr = the ghosted buffer base
+        for r in {(self.rank - 1) % self.world, (self.rank + 1) % self.world}:
+            if r == self.rank:
+                self._peer[r] = ([b.data_ptr() for b in self.bufs], self.local)
+                continue
+            ptrs = []
+            for handle, offset, _ in everyone[r]:
+                base = ctypes.c_void_p()
+                hb = (ctypes.c_ubyte * 64).from_buffer_copy(handle)
+                _native.check(lib.h3_ipc_open(hb, ctypes.byref(base)), "h3_ipc_open")
+                self._opened.append(base.value)
+                ptrs.append(base.value + offset)
+            self._peer[r] = (ptrs, everyone[r][0][2])
+        self._sync = torch.zeros(1, device="cuda")
+
+    def _barrier(self):
+        """Stream-ordered rendezvous: every rank's previous half step is complete (its planes are
+        final and nobody still reads the buffer about to be overwritten)."""
+        if self.world == 1:
+            return
+        if dist.get_backend(self.group) == "nccl":
+            dist.all_reduce(self._sync, group=self.group)
+        else:  # gloo (tests: several ranks sharing one GPU)
+            torch.cuda.synchronize()
+            dist.barrier(group=self.group)
+
+    def _half_p2p(self, si, di, off, flag, timed):
+        m1, m2, _ = self.grid.cells_per_axis
+        h_mat, f1, f2, f3, cf = self._fac
+        src, dst = self.bufs[si], self.bufs[di]
+        plane = src[0].numel() * src.element_size()
+        self._barrier()
+        glo = ghi = None
+        if off == 0:  # cell L-1 reads node plane L = rank+1's first local plane
+            ptrs, _ = self._peer[(self.rank + 1) % self.world]
+            ghi = ctypes.c_void_p(ptrs[si] + plane)
+        else:         # cell 0 reads node plane -1 = rank-1's last local plane
+            ptrs, lprev = self._peer[(self.rank - 1) % self.world]
+            glo = ctypes.c_void_p(ptrs[si] + lprev * plane)
+        stream = torch.cuda.current_stream()
+        e0 = torch.cuda.Event(enable_timing=True) if timed else None
+        if e0 is not None:
+            e0.record(stream)
+        rc = _native.lib().h3_fused_pass_halo(
+            ctypes.c_void_p(src.data_ptr() + plane), ctypes.c_void_p(dst.data_ptr() + plane), m1, m2, self.local,
+            self.order_n, _ptr(h_mat), _ptr(f1), _ptr(f2), _ptr(f3), _ptr(cf), self._q, off, 0, self.local,
+            glo, ghi, _native.VARIANTS[self.cfg.variant], ctypes.c_void_p(stream.cuda_stream),
+            ctypes.c_void_p(flag.data_ptr()), None)
+        _native.check(rc, "h3_fused_pass_halo")
+        if e0 is not None:
+            e1 = torch.cuda.Event(enable_timing=True)
+            e1.record(stream)
+            self.kernel_events.append((e0, e1))
+
+    def close(self) -> None:
+        """Unmap the peer buffers (p2p halo)."""
+        for base in getattr(self, "_opened", []):
+            _native.lib().h3_ipc_close(ctypes.c_void_p(base))
+        self._opened = []
+
     def half_step(self, src, dst, off, flag, timed=False):
         works = exchange_halo(src, off, self.group, async_op=True)
         ev = self.kernel_events if timed else None
@@ -173,6 +307,12 @@ class SlabSolver:
             self._launch(src, dst, off, 0, 1, flag, None)
 
     def step(self, timed=False) -> None:
+        if self.halo == "auto":
+            raise RuntimeError("call init() first (it selects the halo path)")
+        if self.halo == "p2p":
+            self._half_p2p(0, 1, 0, self.flags[0:1], timed)
+            self._half_p2p(1, 0, -1, self.flags[1:2], timed)
+            return
         self.half_step(self.bufs[0], self.bufs[1], 0, self.flags[0:1], timed)
         self.half_step(self.bufs[1], self.bufs[0], -1, self.flags[1:2], timed)
 

@@ -20,7 +20,7 @@ def _free_port():
         return s.getsockname()[1]
 
 
-def _worker(rank, world, port, order_n, cells, steps, result_path):
+def _worker(rank, world, port, order_n, cells, steps, result_path, halo):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
@@ -28,7 +28,7 @@ def _worker(rank, world, port, order_n, cells, steps, result_path):
         from paper_1609_09841_b200.distributed import SlabSolver, slab_bounds
         torch.cuda.set_device(0)
         cfg = hb.StepConfig(variant="separable")
-        solver = SlabSolver(cells, order_n, cfg)
+        solver = SlabSolver(cells, order_n, cfg, halo=halo)
         solver.init(hb.plane_wave())
         for _ in range(steps):
             solver.step()
@@ -49,18 +49,51 @@ def _worker(rank, world, port, order_n, cells, steps, result_path):
             ops = hb.OperatorSet.for_grid(grid, order_n)
             for _ in range(steps):
                 hb.full_step(state, scratch, cfg, ops, dt=solver.dt)
+            want_halo = {"auto": "p2p" if order_n in (3, 5) else "nccl"}.get(halo, halo)
             with open(result_path, "w") as fh:
-                fh.write("ok" if torch.equal(got, state.tensor.cpu()) else "mismatch")
+                fh.write("ok" if torch.equal(got, state.tensor.cpu()) and solver.halo == want_halo else
+                         f"mismatch (halo {solver.halo}: {solver.halo_note})")
         else:
             dist.send(local.contiguous(), dst=0)
+        dist.barrier()  # peers keep their buffers mapped until everyone is done
+        solver.close()
     finally:
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world,order_n,cells", [(2, 3, (16, 14, 12)), (3, 3, (9, 8, 10)), (2, 5, (8, 8, 6)),
-                                                 (2, 1, (10, 9, 7))])
-def test_slab_solver_multi_rank_on_gpu(world, order_n, cells, tmp_path):
+
+
+
+@pytest.mark.parametrize("world,order_n,cells,halo", [(2, 3, (16, 14, 12), "nccl"), (3, 3, (9, 8, 10), "nccl"),
+                                                      (2, 5, (8, 8, 6), "nccl"), (2, 1, (10, 9, 7), "nccl"),
+                                                      (2, 3, (16, 14, 12), "p2p"), (3, 3, (9, 8, 10), "p2p"),
+                                                      (2, 5, (8, 8, 6), "p2p"), (2, 3, (16, 14, 12), "auto"),
+                                                      (2, 1, (10, 9, 7), "auto")])
+def test_slab_solver_multi_rank_on_gpu(world, order_n, cells, halo, tmp_path):
+    """halo="nccl": ghost planes copied by the exchange (staged through gloo here); halo="p2p": the
+    kernel reads the neighbour's plane in place through a CUDA-IPC mapping (here: processes
+    sharing one GPU, so the mapping is same-device)."""
     out = tmp_path / "result.txt"
-    mp.start_processes(_worker, args=(world, _free_port(), order_n, cells, 3, str(out)), nprocs=world,
+    mp.start_processes(_worker, args=(world, _free_port(), order_n, cells, 3, str(out), halo), nprocs=world,
                        join=True, start_method="spawn")
     assert out.read_text() == "ok"
+
+
+@pytest.mark.parametrize("order_n,cells", [(3, (16, 14, 12)), (5, (8, 8, 6))])
+def test_slab_solver_p2p_single_rank(order_n, cells):
+    """One rank: the p2p halo maps the rank's own boundary planes (periodic wrap) -- the
+    ghost-pointer kernel path against the periodic single-field run, bit for bit."""
+    import paper_1609_09841_b200 as hb
+    from paper_1609_09841_b200.distributed import SlabSolver
+    cfg = hb.StepConfig(variant="separable")
+    solver = SlabSolver(cells, order_n, cfg, halo="p2p")
+    solver.init(hb.plane_wave())
+    grid = hb.GridSpec(cells)
+    state = hb.init_field(hb.plane_wave(), grid, order_n)
+    scratch = hb.DofField.zeros(grid.with_parity("dual"), order_n)
+    ops = hb.OperatorSet.for_grid(grid, order_n)
+    for _ in range(3):
+        solver.step()
+        hb.full_step(state, scratch, cfg, ops, dt=solver.dt)
+    solver.check()
+    assert torch.equal(solver.state, state.tensor)
