@@ -284,8 +284,8 @@ def test_slab_range_and_ghost_planes():
     del full_src
 
 
-@pytest.mark.parametrize("cells", [(1, 1, 1), (1, 4, 3), (5, 1, 1), (2, 2, 2), (17, 3, 1)])
-@pytest.mark.parametrize("order_n", [0, 1, 3])
+@pytest.mark.parametrize("cells", [(1, 1, 1), (1, 4, 3), (5, 1, 1), (2, 2, 2), (17, 3, 1), (9, 7, 5), (13, 6, 2)])
+@pytest.mark.parametrize("order_n", [0, 1, 2, 3, 4, 5])
 def test_degenerate_and_ragged_grids(cells, order_n):
     host = np.random.default_rng(5).uniform(-1, 1, (cells[2], cells[1], cells[0]) + (order_n + 1,) * 3)
     grid = hb.GridSpec(cells)
@@ -298,8 +298,8 @@ def test_degenerate_and_ragged_grids(cells, order_n):
         hb.half_step(hb.DofField(grid, order_n, host), dst, hb.StepConfig(variant=variant), ops, dt=dt)
         if variant == "literal":
             assert np.array_equal(dst.data, ref)
-        else:
-            assert rm.rel_err(dst.data, ref) <= 1e-12
+        else:  # one pass on random data; N >= 4: the reference's own FP64 noise (see SEP_TOL)
+            assert rm.rel_err(dst.data, ref) <= {4: 1e-9, 5: 1e-8}.get(order_n, 1e-12)
 
 
 def test_snapshot_round_trip(tmp_path):
