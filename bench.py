@@ -55,6 +55,9 @@ def parse():
     ap.add_argument("--no-extras", action="store_true",
                     help="skip the secondary configs (two-kernel 512^3 / 128^3, m=5 256^3)")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    ap.add_argument("--strong", type=int, default=0, metavar="M",
+                    help="strong scaling: one M^3 grid split over the N ranks (configs[4]: M = 1024 on 8 GPUs); "
+                         "default: weak scaling with --cells^3 per GPU")
     ap.add_argument("--halo", default="auto", choices=["auto", "nccl", "p2p"],
                     help="N>1 halo: in-kernel reads of the neighbour plane over NVLink (p2p), NCCL copy, "
                          "or auto (p2p verified against NCCL at start-up, else NCCL)")
@@ -233,8 +236,9 @@ def main():
     peak_gbs, peak_src = peaks()
 
     if world > 1:
-        solver = hd.SlabSolver((m, m, m * world), order_n, hb.StepConfig(mode=args.mode, variant=args.variant),
-                               lengths=(1.0, 1.0, float(world)), halo=args.halo)
+        gcells = (args.strong,) * 3 if args.strong else (m, m, m * world)
+        solver = hd.SlabSolver(gcells, order_n, hb.StepConfig(mode=args.mode, variant=args.variant),
+                               lengths=(1.0, 1.0, 1.0) if args.strong else (1.0, 1.0, float(world)), halo=args.halo)
         solver.init(hb.plane_wave())
         step_fn = solver.step
         launches_per_step = solver.launches_per_step
@@ -289,12 +293,15 @@ def main():
     if world > 1:
         dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
     ms_max = float(ms_t.item())
-    dofs_per_step = m * m * m * n3 * world
+    dofs_per_step = (args.strong ** 3 if args.strong and world > 1 else m * m * m * world) * n3
     value = dofs_per_step * args.steps / (ms_max / 1e3)
 
     # dominant-kernel roofline: mean launch time of the half-step kernel
     launch_ms = statistics.mean(a.elapsed_time(b) for a, b in kernel_events) if kernel_events else None
-    alg_bytes = 16 * n3 * m * m * m if args.mode == "fused" else 16 * (n3 + (2 * order_n + 2) ** 3) * m ** 3
+    cells_local = dofs_per_step // world // n3
+    if world > 1 and solver.halo != "p2p":  # the timed launch is the interior: L-1 of the L cell planes
+        cells_local = cells_local * (solver.local - 1) // solver.local
+    alg_bytes = 16 * n3 * cells_local if args.mode == "fused" else 16 * (n3 + (2 * order_n + 2) ** 3) * cells_local
     achieved = alg_bytes / (launch_ms / 1e3) / 1e9 if launch_ms else None
 
     flag_bad = int(flags[0].item()) if world == 1 else -1
@@ -302,12 +309,14 @@ def main():
     result = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "scaling": "strong" if args.strong and world > 1 else "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic: plane-wave initial data generated on device (h3_init_separable)",
         "config": {"workload": f"m={order_n}, {m}^3 cells per GPU, {args.mode} "
                                f"{'monolithic' if args.mode == 'fused' else 'two-kernel'} "
                                f"({args.variant}) half-step kernels, periodic advection, cfl 0.9, q={3 * (2 * order_n + 1)}",
-                   "order_m": order_n, "cells_per_gpu": [m, m, m], "global_cells": [m, m, m * world],
+                   "order_m": order_n,
+                   "cells_per_gpu": [args.strong, args.strong, args.strong // world] if args.strong and world > 1 else [m, m, m],
+                   "global_cells": [args.strong] * 3 if args.strong and world > 1 else [m, m, m * world],
                    "mode": args.mode, "variant": args.variant, "parallelism": f"slab-x3 x{world}",
                    "halo": (solver.halo + (f" ({solver.halo_note})" if solver.halo_note else "")) if world > 1 else None,
                    "l2": f"inputs larger than L2 ({dofs_per_step // world * 8 / 1e9:.1f} GB per field vs 126 MB L2)"},
