@@ -28,6 +28,7 @@ Differences that matter to callers:
 from __future__ import annotations
 
 import ctypes
+from collections import OrderedDict
 from dataclasses import dataclass
 
 import numpy as np
@@ -433,9 +434,11 @@ def run_steps(
                      [first_step + k // 2 for k in range(2 * steps)])
 
 
-# captured step blocks, keyed by (fields, config, dt, block length); a graph replays its kernels
-# with the field pointers baked in, so it is only reused for the same state/scratch tensors
-_GRAPHS: dict = {}
+# captured step blocks, keyed by (field addresses and shapes, config, dt, block length): a graph
+# replays its kernels with the field pointers baked in, so it is valid for whatever tensors occupy
+# those addresses with those shapes.  Small LRU (the graphs hold no field references).
+_GRAPHS: "OrderedDict" = None
+_GRAPH_CACHE_SIZE = 16
 
 
 def _run_steps_graph(state, scratch, cfg, ops, steps, dt, first_step, block: int = 32) -> None:
@@ -448,8 +451,13 @@ def _run_steps_graph(state, scratch, cfg, ops, steps, dt, first_step, block: int
         nb = min(block, steps - done)
         key = (state.tensor.data_ptr(), scratch.tensor.data_ptr(), tuple(state.tensor.shape), cfg, ops.order_n,
                float(dt), nb, dev.index)
+        global _GRAPHS
+        if _GRAPHS is None:
+            _GRAPHS = OrderedDict()
         entry = _GRAPHS.get(key)
-        if entry is None:
+        if entry is not None:
+            _GRAPHS.move_to_end(key)
+        else:
             flags = _new_flags(2 * nb, dev)
             g = torch.cuda.CUDAGraph()
             side = torch.cuda.Stream(dev)
@@ -463,7 +471,9 @@ def _run_steps_graph(state, scratch, cfg, ops, steps, dt, first_step, block: int
                     half_step(scratch, state, cfg, ops, dt=dt, _flag=f1, _guard=f0, _check=False)
                     prev = f1
             cur.wait_stream(side)
-            entry = _GRAPHS[key] = (g, flags, state.tensor, scratch.tensor)
+            entry = _GRAPHS[key] = (g, flags)
+            while len(_GRAPHS) > _GRAPH_CACHE_SIZE:
+                _GRAPHS.popitem(last=False)
         g, flags = entry[0], entry[1]
         g.replay()
         host = flags.cpu().numpy()
