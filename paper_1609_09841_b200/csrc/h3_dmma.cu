@@ -103,6 +103,13 @@ struct Dm3Cfg {
     static_assert(STAGES >= 2, "need at least double buffering");
 };
 
+// ~hi(x) & 0x7ff00000 in one LOP3: zero iff x is Inf/NaN (exponent all ones)
+__device__ __forceinline__ unsigned exp_gap(double x) {
+    unsigned r;
+    asm("lop3.b32 %0, %1, 0x7ff00000, 0, 0x0c;" : "=r"(r) : "r"((unsigned)__double2hiint(x)));
+    return r;
+}
+
 template <class C>
 __global__ void __launch_bounds__(C::THREADS, C::MINB)
 sep_fused_dmma3_kernel(const double* __restrict__ src, double* __restrict__ dst, Dims d, int off,
@@ -363,6 +370,9 @@ sep_fused_dmma3_kernel(const double* __restrict__ src, double* __restrict__ dst,
             if constexpr (C::LEAN) {
                 if (pp > 0) {
                     double* oplane = dst + (zc0 + pp - 1) * plane_elems;
+                    // opaque to the optimiser: one 64-bit plane pointer, then one IMAD.WIDE per
+                    // store pair (instead of re-deriving dst + plane + offset per store)
+                    asm volatile("" : "+l"(oplane));
                     unsigned screen = 0x7ff00000u;
 #pragma unroll
                     for (int k = 0; k < K3; ++k) {
@@ -373,8 +383,7 @@ sep_fused_dmma3_kernel(const double* __restrict__ src, double* __restrict__ dst,
                                 __stcs(oplane + ooff[k] + 16, v1[k]);
                             }
                         }
-                        screen = min(screen, min(~(unsigned)__double2hiint(v0[k]) & 0x7ff00000u,
-                                                 ~(unsigned)__double2hiint(v1[k]) & 0x7ff00000u));
+                        screen = min(screen, min(exp_gap(v0[k]), exp_gap(v1[k])));
                     }
                     if (screen == 0u) {  // rare: some lane holds Inf/NaN (finished or partial)
 #pragma unroll
