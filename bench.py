@@ -334,17 +334,37 @@ def main():
     }
     result["clocks"] = clocks.summary()
 
-    # ---- e2e through the package API with host-resident state (1 GPU) ---------------------
+    # ---- e2e through the package API with host-resident state ------------------------------
     print(f"[bench] value {value:.4e} DOF-updates/s, kernel {launch_ms} ms", file=sys.stderr, flush=True)
-    if world == 1 and not args.no_e2e:
-        del scratch
-        scratch = None
-        torch.cuda.empty_cache()
-        try:
-            result["e2e"] = e2e_host(hb, torch, state, grid, order_n, cfg, dt, args.e2e_steps, dofs_per_step)
-        except (RuntimeError, MemoryError) as exc:  # e.g. not enough host RAM for the field
+    if not args.no_e2e:
+        local_bytes = dofs_per_step // world * 8
+        room = host_room(local_bytes)
+        if world > 1:  # every rank must take part (the streamed step exchanges halo planes)
+            ok = torch.tensor([1 if room is None else 0], dtype=torch.int64,
+                              device="cuda" if args.backend == "nccl" else "cpu")
+            dist.all_reduce(ok, op=dist.ReduceOp.MIN)
+            if room is None and int(ok.item()) == 0:
+                room = "another rank lacks host memory for its slab"
+        if room is not None:
             result["e2e"] = {"value": None, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0,
-                             "error": f"{type(exc).__name__}: {exc}"[:300]}
+                             "error": room}
+        else:
+            if world == 1:
+                del scratch
+                scratch = None
+                e2e_args = (state, grid, cfg, dt, None)
+            else:
+                e2e_args = (solver.state, solver.grid, solver.cfg, solver.dt, solver)
+            torch.cuda.empty_cache()
+            try:
+                fstate, fgrid, fcfg, fdt, fsolver = e2e_args
+                del e2e_args
+                result["e2e"] = e2e_host(hb, torch, fstate, fgrid, order_n, fcfg, fdt, args.e2e_steps, dofs_per_step,
+                                         solver=fsolver, dist=dist)
+                del fstate
+            except (RuntimeError, MemoryError, ValueError) as exc:  # e.g. pinning failed, two-pass mode
+                result["e2e"] = {"value": None, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0,
+                                 "error": f"{type(exc).__name__}: {exc}"[:300]}
         print(f"[bench] e2e {result['e2e']}", file=sys.stderr, flush=True)
     # ---- CPU baseline (rank 0, N = 1) ----------------------------------------------------------
     if world == 1 and not args.no_cpu:
@@ -361,32 +381,66 @@ def main():
         dist.destroy_process_group()
 
 
-def e2e_host(hb, torch, state, grid, order_n, cfg, dt, steps, dofs_per_step):
-    """Host-resident state through the package API (HostStepper, the drop-in for the
-    reference's full_step on a host field): every step uploads the whole primary field
-    from pinned host memory, steps it and writes it back, with the transfers and kernels of
-    successive x3 chunks overlapped; the step's result (instability flags) is read back."""
+def host_room(local_bytes):
+    """None when this node's free host memory holds every local rank's pinned field copy
+    (with 25 % headroom), else the reason: pinning more than is free would invite the OOM
+    killer and lose the whole bench line."""
     try:
-        host = torch.empty(state.tensor.shape, dtype=torch.float64, pin_memory=True)
+        with open("/proc/meminfo") as fh:
+            info = {l.split(":")[0]: int(l.split()[1]) * 1024 for l in fh if ":" in l}
+        free = info.get("MemAvailable", 0)
+    except (OSError, ValueError):
+        return "cannot read /proc/meminfo"
+    ranks_here = int(os.environ.get("LOCAL_WORLD_SIZE", "1"))
+    need = int(1.25 * local_bytes * ranks_here)
+    return None if need <= free else f"host memory: {need / 1e9:.0f} GB needed, {free / 1e9:.0f} GB available"
+
+
+def e2e_host(hb, torch, state, grid, order_n, cfg, dt, steps, dofs_per_step, solver=None, dist=None):
+    """Host-resident state through the package API (HostStepper, the drop-in for the
+    reference's full_step on a host field): every step uploads the whole primary field (N > 1:
+    each rank its x3 slab) from pinned host memory, steps it and writes it back, with the
+    transfers and kernels of successive x3 chunks overlapped and (N > 1) the slab halo planes
+    exchanged over NCCL; the step's result (instability flags) is read back.  Wall time, max
+    over ranks."""
+    dof_field = state if solver is None else None
+    src = state.tensor if solver is None else state
+    try:
+        host = torch.empty(src.shape, dtype=torch.float64, pin_memory=True)
         pinned = True
     except RuntimeError:
-        host = torch.empty(state.tensor.shape, dtype=torch.float64)
+        host = torch.empty(src.shape, dtype=torch.float64)
         pinned = False
-    host.copy_(state.tensor)
-    state.tensor = None  # free HBM: the streamed step keeps only a few chunks on the device
+    host.copy_(src)
+    del src, state  # (a slab view keeps the solver's field alive until the caller drops it: HBM has room)
+    if solver is None:
+        dof_field.tensor = None  # free HBM: the streamed step keeps only a few chunks on the device
+    else:
+        solver.close()
+        solver.bufs = None
     torch.cuda.empty_cache()
+    world = dist.get_world_size() if solver is not None else 1
     stepper = hb.HostStepper(host, grid, order_n, cfg)
     stepper.step(dt=dt)  # warm-up (allocations, first launches)
     torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
     t0 = time.perf_counter()
     for k in range(steps):
         stepper.step(dt=dt, step_index=k)  # ends with the D2H read of the step's flags
     wall = time.perf_counter() - t0
-    return {"value": dofs_per_step * steps / wall, "unit": UNIT, "h2d_bytes_per_step": stepper.h2d_bytes,
-            "d2h_bytes_per_step": stepper.d2h_bytes + 16 * len(stepper.chunks), "steps": steps, "pinned": pinned,
-            "chunks": len(stepper.chunks),
+    if world > 1:
+        w = torch.tensor([wall], dtype=torch.float64,
+                         device="cuda" if dist.get_backend() == "nccl" else "cpu")
+        dist.all_reduce(w, op=dist.ReduceOp.MAX)
+        wall = float(w.item())
+    return {"value": dofs_per_step * steps / wall, "unit": UNIT, "h2d_bytes_per_step": stepper.h2d_bytes * world,
+            "d2h_bytes_per_step": (stepper.d2h_bytes + 16 * len(stepper.chunks)) * world, "steps": steps,
+            "pinned": pinned, "chunks": len(stepper.chunks), "wall_s": wall,
             "api": "paper_1609_09841_b200.HostStepper.step on a host-resident field (chunked H2D -> fused "
-                   "half steps -> D2H, overlapped on three streams)"}
+                   "half steps -> D2H, overlapped on three streams"
+                   + (f"; {world} ranks, each streaming its x3 slab, halo planes over "
+                      f"{dist.get_backend()})" if world > 1 else ")")}
 
 
 def extras(hb, torch, order_n, peak_gbs):

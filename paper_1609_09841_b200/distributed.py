@@ -39,7 +39,7 @@ from . import _native
 from .field import GridSpec
 from .pipeline import InstabilityError, OperatorSet, StepConfig, _factor_arrays, _node_of, _ptr, select_dt
 
-__all__ = ["slab_bounds", "halo_plan", "exchange_halo", "SlabSolver"]
+__all__ = ["slab_bounds", "halo_plan", "exchange_halo", "agree_first_bad", "SlabSolver"]
 
 
 def slab_bounds(m3: int, world: int, rank: int) -> tuple[int, int]:
@@ -92,6 +92,29 @@ def exchange_halo(buf: torch.Tensor, off: int, group=None, async_op: bool = Fals
     for w in works:
         w.wait()
     return []
+
+
+def agree_first_bad(per_half: list[int], group=None, device=None) -> list[int]:
+    """Make an instability report collective: `per_half` holds, for each half step in order,
+    this rank's first non-finite node as a GLOBAL linear index ((m3 M2 + m2) M1 + m1, the
+    reference's C-order scan) or -1; returns the minimum over all ranks per half step, so
+    every rank raises the same InstabilityError (and none is left waiting in the next step's
+    halo exchange)."""
+    if not dist.is_initialized() or dist.get_world_size(group) == 1:
+        return list(per_half)
+    big = np.iinfo(np.int64).max
+    dev = device if dist.get_backend(group) == "nccl" else "cpu"
+    t = torch.tensor([v if v >= 0 else big for v in per_half], dtype=torch.int64, device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MIN, group=group)
+    return [int(v) if int(v) != big else -1 for v in t.cpu()]
+
+
+def raise_first_bad(per_half: list[int], grid: GridSpec, step_index) -> None:
+    """Raise the reference's InstabilityError for the first half step with a bad node."""
+    m1, m2, _ = grid.cells_per_axis
+    for idx in per_half:
+        if idx >= 0:
+            raise InstabilityError(_node_of(idx, GridSpec((m1, m2, grid.cells_per_axis[2]))), step_index)
 
 
 class SlabSolver:
@@ -317,9 +340,10 @@ class SlabSolver:
         self.half_step(self.bufs[1], self.bufs[0], -1, self.flags[1:2], timed)
 
     def check(self, step_index=None) -> None:
-        host = self.flags.cpu().numpy()
-        for k, bad in enumerate(host):
-            if int(bad) != -1:
-                m1, m2, _ = self.grid.cells_per_axis
-                x, y, z = _node_of(int(bad), GridSpec((m1, m2, self.local)))
-                raise InstabilityError((x, y, z + self.z0), step_index)
+        """Raise InstabilityError on EVERY rank when any rank has produced a non-finite value
+        (flags are sticky: call after each step; the first bad node over the whole grid, in
+        half-step order)."""
+        m1, m2, _ = self.grid.cells_per_axis
+        plane = m1 * m2
+        local = [int(b) + self.z0 * plane if int(b) != -1 else -1 for b in self.flags.cpu().numpy()]
+        raise_first_bad(agree_first_bad(local, self.group, self.flags.device), self.grid, step_index)

@@ -20,6 +20,13 @@ and a device copy of the original plane 0 serves as the ghost of chunk K-1.  The
 planes are copied device to device from the next chunk's upload, so every primary plane crosses
 PCIe exactly once in each direction.
 
+Slabs (multi-GPU, one rank per GPU): with a torch.distributed process group of more than one
+rank, each rank streams its own x3 slab of the global grid (`distributed.slab_bounds`) and the
+two wrap-around planes become the slab halo: the rank's original first plane goes to rank-1
+and rank+1's arrives as the ghost of the last dual chunk (one exchange at the start of the
+step), and the last dual plane goes to rank+1 while rank-1's arrives as the ghost of primary
+chunk 0 (one exchange before it is finished) -- NCCL send/recv on the compute stream.
+
 Each chunk is a slab with ghost planes, stepped by the same C-ABI half step as the
 single-field path (h3_fused_pass with periodic_z = 0), so results are bit-identical to
 `full_step` on a device-resident field.  Instabilities raise the reference's
@@ -33,6 +40,7 @@ import ctypes
 
 import numpy as np
 import torch
+import torch.distributed as dist
 
 from . import _native
 from .field import GridSpec
@@ -57,15 +65,29 @@ class HostStepper:
     """Streamed full steps of a pinned host field (M3, M2, M1, n, n, n), updated in place."""
 
     def __init__(self, host_state: torch.Tensor, grid: GridSpec, order_n: int, cfg: StepConfig | None = None,
-                 chunk_planes: int | None = None, device=None):
+                 chunk_planes: int | None = None, device=None, group=None):
+        """`grid` is the global grid.  Without a multi-rank process group `host_state` is the
+        whole field (M3, M2, M1, n, n, n); with one (`group`, default: the default group when
+        torch.distributed is initialised) it is this rank's slab (z1 - z0, M2, M1, n, n, n),
+        [z0, z1) = distributed.slab_bounds(M3, world, rank)."""
         cfg = cfg or StepConfig()
         if cfg.mode != "fused" or cfg.precision != "double":
             raise ValueError("HostStepper streams the fused FP64 half step")
         m1, m2, m3 = grid.cells_per_axis
         n = order_n + 1
-        if host_state.device.type != "cpu" or tuple(host_state.shape) != (m3, m2, m1, n, n, n) \
+        self.group = group
+        self.world = dist.get_world_size(group) if dist.is_initialized() else 1
+        self.rank = dist.get_rank(group) if dist.is_initialized() else 0
+        if self.world > 1:
+            from .distributed import slab_bounds
+            self.z0, z1 = slab_bounds(m3, self.world, self.rank)
+            planes = z1 - self.z0
+        else:
+            self.z0, planes = 0, m3
+        if host_state.device.type != "cpu" or tuple(host_state.shape) != (planes, m2, m1, n, n, n) \
                 or host_state.dtype != torch.float64 or not host_state.is_contiguous():
-            raise ValueError("host_state must be a contiguous CPU float64 tensor of shape (M3, M2, M1, n, n, n)")
+            raise ValueError(f"host_state must be a contiguous CPU float64 tensor of shape "
+                             f"{(planes, m2, m1, n, n, n)} (this rank's x3 planes, M2, M1, n, n, n)")
         self.host = host_state
         self.pinned = host_state.is_pinned()
         self.grid = grid.with_parity("primary")
@@ -76,7 +98,7 @@ class HostStepper:
         plane = m1 * m2 * n ** 3
         if chunk_planes is None:  # ~2 GB chunks: measured best at 512^3 (tools/time_stream.py)
             chunk_planes = max(2, (2 << 30) // (plane * 8))
-        self.chunks = chunk_plan(m3, chunk_planes)
+        self.chunks = chunk_plan(planes, chunk_planes)
         cmax = max(z1 - z0 for z0, z1 in self.chunks)
         kw = dict(dtype=torch.float64, device=self.device)
         shape = lambda planes: (planes, m2, m1, n, n, n)  # noqa: E731
@@ -85,11 +107,12 @@ class HostStepper:
         self.dual0 = torch.empty(shape(self.chunks[0][1] + 1), **kw)         # dual chunk 0 (kept)
         self.pout = [torch.empty(shape(cmax), **kw) for _ in range(2)]
         self.plane0 = torch.empty(shape(1)[1:], **kw)
+        self.ghost_hi = torch.empty(shape(1)[1:], **kw) if self.world > 1 else self.plane0
         self.s_h2d = torch.cuda.Stream(self.device)
         self.s_cmp = torch.cuda.Stream(self.device)
         self.s_d2h = torch.cuda.Stream(self.device)
-        self.h2d_bytes = m3 * plane * 8
-        self.d2h_bytes = m3 * plane * 8
+        self.h2d_bytes = planes * plane * 8
+        self.d2h_bytes = planes * plane * 8
         self._plane = plane
 
     # -- one half step on a slab with ghost planes (h3_fused_pass, periodic_z = 0) --------------
@@ -102,6 +125,22 @@ class HostStepper:
             self.cfg.stages(self.order_n), off, 0, planes, 0, _native.VARIANTS[self.cfg.variant],
             ctypes.c_void_p(self.s_cmp.cuda_stream), ctypes.c_void_p(flag.data_ptr()), None)
         _native.check(rc, "h3_fused_pass (streamed chunk)")
+
+    def _swap(self, send: torch.Tensor, send_to: int, recv: torch.Tensor, recv_from: int) -> None:
+        """Send one plane to a neighbour rank and receive one, ordered on the compute stream."""
+        g = self.group
+        to_g = dist.get_global_rank(g, send_to) if g is not None else send_to
+        from_g = dist.get_global_rank(g, recv_from) if g is not None else recv_from
+        if dist.get_backend(g) == "gloo":  # host staging (tests of the multi-rank path on one GPU)
+            host_send, host_recv = send.cpu(), torch.empty(recv.shape, dtype=recv.dtype)
+            for w in dist.batch_isend_irecv([dist.P2POp(dist.isend, host_send, to_g, g),
+                                             dist.P2POp(dist.irecv, host_recv, from_g, g)]):
+                w.wait()
+            recv.copy_(host_recv)
+            return
+        for w in dist.batch_isend_irecv([dist.P2POp(dist.isend, send, to_g, g),
+                                         dist.P2POp(dist.irecv, recv, from_g, g)]):
+            w.wait()  # NCCL: makes the current (compute) stream wait, not the host
 
     def step(self, dt: float | None = None, step_index: int | None = None) -> None:
         """One full step (primary -> dual -> primary) of the host field, in place."""
@@ -152,6 +191,11 @@ class HostStepper:
                 pout_free[k % 2] = e
 
         up = upload(0)
+        nxt_rank, prv_rank = (self.rank + 1) % self.world, (self.rank - 1) % self.world
+        if self.world > 1:  # my original first plane -> rank-1, rank+1's -> ghost of the last dual chunk
+            with torch.cuda.stream(self.s_cmp):
+                self.s_cmp.wait_event(up)
+                self._swap(self.plane0, prv_rank, self.ghost_hi, nxt_rank)
         for k in range(K):
             nxt = upload(k + 1) if k + 1 < K else None
             z0, z1 = self.chunks[k]
@@ -165,7 +209,7 @@ class HostStepper:
                     self.s_cmp.wait_event(nxt)
                     self.pin[k % 2][L].copy_(self.pin[(k + 1) % 2][0])
                 else:
-                    self.pin[k % 2][L].copy_(self.plane0)
+                    self.pin[k % 2][L].copy_(self.ghost_hi)
                 self._half(self.pin[k % 2], dst[1:], L, 0, fac, flags[0, k])
                 e = ev()
                 e.record(self.s_cmp)
@@ -177,11 +221,14 @@ class HostStepper:
             if k >= 1:
                 finish(k, dst)
             up = nxt
-        # primary chunk 0 last: its ghost is the last dual plane of chunk K-1
+        # primary chunk 0 last: its ghost is the last dual plane of chunk K-1 (of rank-1 for slabs)
         with torch.cuda.stream(self.s_cmp):
             last = self.dual0 if K == 1 else self.dbuf[(K - 1) % 2]
             lp = self.chunks[K - 1][1] - self.chunks[K - 1][0]
-            self.dual0[0].copy_(last[lp])
+            if self.world > 1:
+                self._swap(last[lp], nxt_rank, self.dual0[0], prv_rank)
+            else:
+                self.dual0[0].copy_(last[lp])
         finish(0, self.dual0)
         for s in (self.s_h2d, self.s_cmp, self.s_d2h):
             cur.wait_stream(s)
@@ -190,13 +237,18 @@ class HostStepper:
 
     def _raise(self, host_flags, step_index):
         m1, m2, _ = self.grid.cells_per_axis
-        for half, parity in ((0, "dual"), (1, "primary")):
-            best = None
-            for k, (z0, z1) in enumerate(self.chunks):
+        per_half = []
+        for half in (0, 1):  # dual, then primary: the reference raises after the first bad half step
+            best = -1
+            for k, (z0, _z1) in enumerate(self.chunks):
                 bad = int(host_flags[half, k])
                 if bad != -1:
-                    x, y, z = _node_of(bad, GridSpec((m1, m2, z1 - z0)))
-                    cand = (z + z0, y, x)
-                    best = cand if best is None or cand < best else best
-            if best is not None:
-                raise InstabilityError(node=(best[2], best[1], best[0]), step=step_index)
+                    idx = bad + (z0 + self.z0) * m1 * m2  # chunk-local C-order index -> global
+                    best = idx if best == -1 else min(best, idx)
+            per_half.append(best)
+        if self.world > 1:
+            from .distributed import agree_first_bad
+            per_half = agree_first_bad(per_half, self.group, self.device)
+        for idx in per_half:
+            if idx != -1:
+                raise InstabilityError(node=_node_of(idx, self.grid), step=step_index)

@@ -92,3 +92,22 @@ def _worker(rank, world, port, order_n, cells, steps, q):
 def test_slab_halo_exchange_matches_single_field(world, cells, order_n):
     mp.start_processes(_worker, args=(world, _free_port(), order_n, cells, 3, None), nprocs=world,
                        join=True, start_method="spawn")
+
+
+def _agree_worker(rank, world, port, per_rank, want):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_1609_09841_b200.distributed import agree_first_bad
+        got = agree_first_bad(per_rank[rank])
+        assert got == want, (rank, got, want)
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("per_rank,want", [([[-1, 7], [12, -1]], [12, 7]), ([[-1, -1], [-1, -1]], [-1, -1]),
+                                           ([[30, 9], [4, 11]], [4, 9])])
+def test_instability_agreement_is_min_over_ranks(per_rank, want):
+    """Every rank gets the first bad global node per half step (min over ranks, -1 = none)."""
+    mp.start_processes(_agree_worker, args=(2, _free_port(), per_rank, want), nprocs=2, join=True,
+                       start_method="spawn")

@@ -97,3 +97,50 @@ def test_slab_solver_p2p_single_rank(order_n, cells):
         hb.full_step(state, scratch, cfg, ops, dt=solver.dt)
     solver.check()
     assert torch.equal(solver.state, state.tensor)
+
+
+def _bad_worker(rank, world, port, cells, bad, halo, result_path):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import paper_1609_09841_b200 as hb
+        from paper_1609_09841_b200.distributed import SlabSolver
+        torch.cuda.set_device(0)
+        cfg = hb.StepConfig(variant="separable")
+        solver = SlabSolver(cells, 3, cfg, halo=halo)
+        solver.init(hb.plane_wave())
+        if solver.z0 <= bad[0] < solver.z1:
+            solver.state[(bad[0] - solver.z0,) + tuple(bad[1:])] = float("inf")
+        err = None
+        try:
+            solver.step()
+            solver.check(step_index=4)
+        except hb.InstabilityError as e:
+            err = (e.node, e.step)
+        errs = [None] * world
+        dist.all_gather_object(errs, err)
+        if rank == 0:
+            grid = hb.GridSpec(cells)
+            state = hb.init_field(hb.plane_wave(), grid, 3)
+            state.tensor[bad] = float("inf")
+            scratch = hb.DofField.zeros(grid.with_parity("dual"), 3)
+            with pytest.raises(hb.InstabilityError) as ref:
+                hb.full_step(state, scratch, cfg, hb.OperatorSet.for_grid(grid, 3), dt=solver.dt, step_index=4)
+            want = (ref.value.node, ref.value.step)
+            with open(result_path, "w") as fh:
+                fh.write("ok" if all(e == want for e in errs) else f"mismatch {errs} vs {want}")
+        dist.barrier()
+        solver.close()
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("halo", ["nccl", "p2p"])
+def test_slab_solver_instability_is_collective(halo, tmp_path):
+    """A non-finite value on one rank makes EVERY rank raise the same InstabilityError (the
+    first bad node of the whole grid, as full_step reports it), so no rank is left waiting in
+    the next halo exchange."""
+    out = tmp_path / "result.txt"
+    mp.start_processes(_bad_worker, args=(2, _free_port(), (8, 7, 8), (5, 2, 3, 0, 0, 0), halo, str(out)),
+                       nprocs=2, join=True, start_method="spawn")
+    assert out.read_text() == "ok"
