@@ -9,10 +9,13 @@
 // cudaMemcpyToSymbolAsync on the caller's stream when no slot matches, then recording the slot's
 // `ready` event; a caller on another stream that finds the slot waits on that event);
 // cop_release() records the launch's completion event on the slot.  A slot is overwritten only
-// after every recorded user has completed (the uploading stream waits on their events).
+// after every recorded user has completed (the uploading stream waits on their events), and never
+// while a caller holds it between acquire and release (its launch is not recorded yet): such
+// slots are skipped, and if all are held the caller waits for one to be released.
 #pragma once
 #include <cuda_runtime.h>
 
+#include <condition_variable>
 #include <cstring>
 #include <mutex>
 #include <type_traits>
@@ -54,6 +57,7 @@ struct CopSlotState {
     double bits[COP_SLOT];
     std::vector<cudaEvent_t> users;
     cudaEvent_t ready = nullptr;  // recorded after the upload; other streams wait on it
+    int held = 0;                 // callers between cop_acquire and cop_release
 };
 struct CopDeviceState {
     CopSlotState slot[COP_SLOTS];
@@ -64,6 +68,10 @@ constexpr int COP_MAX_DEVICES = 64;
 static std::mutex& cop_mutex() {
     static std::mutex m;
     return m;
+}
+static std::condition_variable& cop_released() {
+    static std::condition_variable cv;
+    return cv;
 }
 static CopDeviceState& cop_device(int dev) {
     static CopDeviceState states[COP_MAX_DEVICES];
@@ -77,7 +85,7 @@ static int cop_acquire(const double* ops, int count, cudaStream_t st, int* slot)
     cudaError_t e = cudaGetDevice(&dev);
     if (e != cudaSuccess) return (int)e;
     if (dev < 0 || dev >= COP_MAX_DEVICES) return (int)cudaErrorInvalidDevice;
-    std::lock_guard<std::mutex> lk(cop_mutex());
+    std::unique_lock<std::mutex> lk(cop_mutex());
     CopDeviceState& D = cop_device(dev);
     for (int s = 0; s < COP_SLOTS; ++s)
         if (D.slot[s].count == count && std::memcmp(D.slot[s].bits, ops, count * sizeof(double)) == 0) {
@@ -86,10 +94,19 @@ static int cop_acquire(const double* ops, int count, cudaStream_t st, int* slot)
                 e = cudaStreamWaitEvent(st, D.slot[s].ready, 0);
                 if (e != cudaSuccess) return (int)e;
             }
+            ++D.slot[s].held;
             *slot = s;
             return 0;
         }
-    const int s = D.next;
+    int s = -1;
+    for (;;) {  // next slot in ring order that no caller holds
+        for (int i = 0; i < COP_SLOTS && s < 0; ++i) {
+            const int c = (D.next + i) % COP_SLOTS;
+            if (D.slot[c].held == 0) s = c;
+        }
+        if (s >= 0) break;
+        cop_released().wait(lk);  // all COP_SLOTS held by concurrent callers: wait for a release
+    }
     D.next = (s + 1) % COP_SLOTS;
     CopSlotState& S = D.slot[s];
     for (cudaEvent_t ev : S.users) {
@@ -110,6 +127,7 @@ static int cop_acquire(const double* ops, int count, cudaStream_t st, int* slot)
     if (e != cudaSuccess) return (int)e;
     std::memcpy(S.bits, ops, count * sizeof(double));
     S.count = count;
+    ++S.held;
     *slot = s;
     return 0;
 }
@@ -120,6 +138,7 @@ static int cop_release(int slot, cudaStream_t st) {
     if (e != cudaSuccess) return (int)e;
     std::lock_guard<std::mutex> lk(cop_mutex());
     CopSlotState& S = cop_device(dev).slot[slot];
+    if (S.held > 0 && --S.held == 0) cop_released().notify_all();
     // drop completed users so the list stays short
     size_t keep = 0;
     for (size_t i = 0; i < S.users.size(); ++i) {

@@ -425,6 +425,55 @@ def test_constant_operator_ring_cross_stream_upload_order():
             assert rm.rel_err(o.cpu().numpy(), ref.cpu().numpy()) <= 1e-13
 
 
+def test_constant_operator_ring_concurrent_host_threads():
+    """Eight host threads (ctypes drops the GIL), each on its own stream with its own operator
+    set -- twice as many sets as constant slots: a slot held between acquire and release is
+    never recycled under another thread's launch, so every launch sees its own operators."""
+    import threading
+    n = 1
+    nn = n + 1
+    src = torch.from_numpy(np.random.default_rng(9).uniform(-1, 1, (4, 5, 6, nn, nn, nn))).cuda()
+    base = np.ascontiguousarray(rm.interp_matrix(n))
+    lib = _native.lib()
+    hs = [np.ascontiguousarray(base * (1.0 + 0.21 * (k + 1))) for k in range(8)]
+    refs = []
+    for h in hs:
+        ref = torch.empty((4, 5, 6, 4, 4, 4), dtype=torch.float64, device="cuda")
+        assert lib.h3_recon_pass(ctypes.c_void_p(src.data_ptr()), ctypes.c_void_p(ref.data_ptr()), 6, 5, 4, n,
+                                 h.ctypes.data_as(ctypes.c_void_p), 0, 0, 4, 1, _native.VARIANTS["literal"],
+                                 None, None) == 0
+        refs.append(ref)
+    torch.cuda.synchronize()
+    streams = [torch.cuda.Stream() for _ in hs]
+    outs = [[] for _ in hs]
+    errors = []
+
+    def work(k):
+        try:
+            torch.cuda.set_device(0)
+            for _ in range(25):
+                coeff = torch.empty((4, 5, 6, 4, 4, 4), dtype=torch.float64, device="cuda")
+                rc = lib.h3_recon_pass(ctypes.c_void_p(src.data_ptr()), ctypes.c_void_p(coeff.data_ptr()),
+                                       6, 5, 4, n, hs[k].ctypes.data_as(ctypes.c_void_p), 0, 0, 4, 1,
+                                       _native.VARIANTS["separable"], ctypes.c_void_p(streams[k].cuda_stream), None)
+                if rc:
+                    errors.append(rc)
+                outs[k].append(coeff)
+        except Exception as exc:  # noqa: BLE001
+            errors.append(exc)
+
+    threads = [threading.Thread(target=work, args=(k,)) for k in range(len(hs))]
+    for t in threads:
+        t.start()
+    for t in threads:
+        t.join()
+    torch.cuda.synchronize()
+    assert not errors
+    for k, ref in enumerate(refs):
+        for o in outs[k]:
+            assert rm.rel_err(o.cpu().numpy(), ref.cpu().numpy()) <= 1e-13
+
+
 @pytest.mark.parametrize("order_n,cells,steps", [(3, (12, 10, 9), 37), (5, (8, 8, 6), 9), (1, (16, 16, 16), 40)])
 def test_run_steps_graph_replay_bitwise(order_n, cells, steps):
     """CUDA-graph replay of run_steps equals the eager launches bit for bit (several blocks and a
