@@ -38,6 +38,13 @@ using tma::mbar_fence_init;
 using tma::mbar_init;
 using tma::mbar_wait;
 
+// group `warp + WARPS * it` of a pass with G groups of 8 lines exists (warp-uniform; constant
+// true when the groups divide evenly, so the unrolled loops keep no test)
+template <int G, int WARPS>
+__device__ __forceinline__ bool live(int warp, int it) {
+    return G % WARPS == 0 || warp + WARPS * it < G;
+}
+
 template <int N_, int TX_, int TY_, int WARPS_ = 16, int STAGES_ = 3, int MINB_ = 1>
 struct Cfg {
     static constexpr int N = N_, n = N + 1, n2 = n * n, n3 = n2 * n, K2 = 2 * n;
@@ -194,12 +201,13 @@ sep_fused_dmma_cp_kernel(const double* __restrict__ src, double* __restrict__ ds
 #pragma unroll
             for (int it = 0; it < I3; ++it) {
                 d[it][0] = d[it][1] = 0.0;
+                if (!live<C::G3, WARPS>(warp, it)) continue;  // warp-uniform: no dummy DMMAs
 #pragma unroll
                 for (int ks = 0; ks < KS; ++ks) dmma(d[it][0], d[it][1], vk[ks][r3[it]], bop[2][ks]);
             }
 #pragma unroll
             for (int it = 0; it < I3; ++it)
-                if (o3[it] >= 0) {
+                if (live<C::G3, WARPS>(warp, it) && o3[it] >= 0) {
                     __stcs(oplane + o3[it], d[it][0]);
                     __stcs(oplane + o3[it] + n2, d[it][1]);
                     if (!isfinite(d[it][0]) || !isfinite(d[it][1]))
@@ -214,12 +222,13 @@ sep_fused_dmma_cp_kernel(const double* __restrict__ src, double* __restrict__ ds
 #pragma unroll
             for (int it = 0; it < I1; ++it) {
                 d[it][0] = d[it][1] = 0.0;
+                if (!live<C::G1, WARPS>(warp, it)) continue;
 #pragma unroll
                 for (int ks = 0; ks < KS; ++ks) dmma(d[it][0], d[it][1], Ub[r1[it] + k1[ks]], bop[0][ks]);
             }
 #pragma unroll
             for (int it = 0; it < I1; ++it)
-                if (w1[it] >= 0) {
+                if (live<C::G1, WARPS>(warp, it) && w1[it] >= 0) {
                     W[w1[it]] = d[it][0];
                     W[w1[it] + WM] = d[it][1];
                 }
@@ -234,12 +243,13 @@ sep_fused_dmma_cp_kernel(const double* __restrict__ src, double* __restrict__ ds
 #pragma unroll
             for (int it = 0; it < I2; ++it) {
                 d[it][0] = d[it][1] = 0.0;
+                if (!live<C::G2, WARPS>(warp, it)) continue;
 #pragma unroll
                 for (int ks = 0; ks < KS; ++ks) dmma(d[it][0], d[it][1], W[r2[it] + k2[ks]], bop[1][ks]);
             }
 #pragma unroll
             for (int it = 0; it < I2; ++it)
-                if (w2[it] >= 0) {
+                if (live<C::G2, WARPS>(warp, it) && w2[it] >= 0) {
                     Vc[w2[it]] = d[it][0];
                     Vc[w2[it] + n] = d[it][1];
                 }
@@ -444,6 +454,7 @@ recon_dmma_cp_kernel(const double* __restrict__ src, double* __restrict__ coeff,
             double* oplane = coeff + (zc0 - d.z_begin + cp) * cplane;
 #pragma unroll
             for (int it = 0; it < I3; ++it) {
+                if (!live<C::G3, WARPS>(warp, it)) continue;  // warp-uniform: no dummy DMMAs
                 double a[KS];
 #pragma unroll
                 for (int ks = 0; ks < KS; ++ks) a[ks] = vk[ks][r3[it]];
@@ -464,6 +475,7 @@ recon_dmma_cp_kernel(const double* __restrict__ src, double* __restrict__ coeff,
         // ---- x1: U(p) -> W[row][cell][i1][j3 j2] ----------------------------------------------
 #pragma unroll
         for (int it = 0; it < I1; ++it) {
+            if (!live<C::G1, WARPS>(warp, it)) continue;
             double a[KS];
 #pragma unroll
             for (int ks = 0; ks < KS; ++ks) a[ks] = Ub[r1[it] + k1[ks]];
@@ -485,6 +497,7 @@ recon_dmma_cp_kernel(const double* __restrict__ src, double* __restrict__ coeff,
         // ---- x2: W -> V[p & 1][cell][j3][i2 i1] -------------------------------------------------
 #pragma unroll
         for (int it = 0; it < I2; ++it) {
+            if (!live<C::G2, WARPS>(warp, it)) continue;
             double a[KS];
 #pragma unroll
             for (int ks = 0; ks < KS; ++ks) a[ks] = W[r2[it] + k2[ks]];
