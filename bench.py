@@ -304,7 +304,14 @@ def main():
     alg_bytes = 16 * n3 * cells_local if args.mode == "fused" else 16 * (n3 + (2 * order_n + 2) ** 3) * cells_local
     achieved = alg_bytes / (launch_ms / 1e3) / 1e9 if launch_ms else None
 
-    flag_bad = int(flags[0].item()) if world == 1 else -1
+    if world == 1:
+        finite = int(flags[0].item()) == -1
+    else:
+        try:
+            solver.check()  # collective: every rank sees the same verdict
+            finite = True
+        except hb.InstabilityError:
+            finite = False
     traffic, traffic_src = measured_traffic(order_n, m, args.mode, args.variant)
     result = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
@@ -330,7 +337,7 @@ def main():
                      "algorithmic_bytes_per_launch": alg_bytes, "mean_launch_ms": launch_ms,
                      "peak_source": peak_src},
         "gpu_launches": launches_per_step * args.steps,
-        "finite": flag_bad == -1,
+        "finite": finite,
     }
     result["clocks"] = clocks.summary()
 
