@@ -77,7 +77,10 @@ int h3_fused_pass_f32(const float* src, float* dst, int64_t M1, int64_t M2, int6
  * the multi-GPU solver, the neighbour rank's boundary plane mapped through CUDA IPC, read in
  * place over NVLink by the kernel's TMA plane loads (no separate halo copy).  Separable variant,
  * N = 3 and 5 (H3_ERR_VARIANT otherwise).  Synchronising the neighbours (the plane must be final
- * before it is read and not rewritten while it is read) is the caller's job. */
+ * before it is read and not rewritten while it is read) is the caller's job.  Same per-cell
+ * contract as fused_pass (reference gridkernels.py:121-139, gather offsets :42-55); the reference
+ * has no multi-process path, this is the slab form SURVEY 8(b)/(e) asks for
+ * ("h3_fused_half_step_dist or a separate halo call"). */
 int h3_fused_pass_halo(const double* src, double* dst, int64_t M1, int64_t M2, int64_t M3,
                        int order_n, const double* h_mat, const double* fac1, const double* fac2,
                        const double* fac3, const double* cfac, int q, int off, int64_t z_begin,
