@@ -257,6 +257,7 @@ class SlabSolver:
         else:
             everyone = [mine]
         self._opened = []
+        bases = {}  # IPC handle -> mapped allocation base
         self._peer = {}  # rank -> ([buf0 ptr, buf1 ptr], local planes); ptr = the ghosted buffer base
         for r in {(self.rank - 1) % self.world, (self.rank + 1) % self.world}:
             if r == self.rank:
@@ -264,11 +265,13 @@ class SlabSolver:
                 continue
             ptrs = []
             for handle, offset, _ in everyone[r]:
-                base = ctypes.c_void_p()
-                hb = (ctypes.c_ubyte * 64).from_buffer_copy(handle)
-                _native.check(lib.h3_ipc_open(hb, ctypes.byref(base)), "h3_ipc_open")
-                self._opened.append(base.value)
-                ptrs.append(base.value + offset)
+                if handle not in bases:  # both fields may live in one allocation: map it once
+                    base = ctypes.c_void_p()
+                    hb = (ctypes.c_ubyte * 64).from_buffer_copy(handle)
+                    _native.check(lib.h3_ipc_open(hb, ctypes.byref(base)), "h3_ipc_open")
+                    self._opened.append(base.value)
+                    bases[handle] = base.value
+                ptrs.append(bases[handle] + offset)
             self._peer[r] = (ptrs, everyone[r][0][2])
         self._sync = torch.zeros(1, device="cuda")
 
