@@ -172,6 +172,18 @@ def cpu_oracle_rate(order_n, cells, seconds_budget):
                   f"CPU throughput is grid-size independent), {wall:.1f} s"}
 
 
+def cpu_model():
+    """Host CPU model name (the reference's perf report names it: SURVEY 8(d))."""
+    try:
+        with open("/proc/cpuinfo") as fh:
+            for line in fh:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return None
+
+
 def cpu_sample_cells(order_n):
     return {0: (128,) * 3, 1: (64,) * 3, 2: (48,) * 3, 3: (48,) * 3, 4: (32,) * 3, 5: (24,) * 3}[order_n]
 
@@ -201,7 +213,7 @@ def run_reference(args, rank, world):
         "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic (plane wave)",
         "config": {"workload": f"m={order_n} {args.cells}^3 periodic advection, reference CPU algorithm",
                    "order_m": order_n, "cells": args.cells, "sampled_cells": list(cells)},
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": info["cores"], "kind": "port",
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": info["cores"], "kind": "port", "cpu": cpu_model(),
                          "sample": info["sample"]},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "gpu_launches": 0,
@@ -376,7 +388,7 @@ def main():
     # ---- CPU baseline (rank 0, N = 1) ----------------------------------------------------------
     if world == 1 and not args.no_cpu:
         rate, info = cpu_oracle_rate(order_n, cpu_sample_cells(order_n), args.cpu_seconds)
-        result["cpu_baseline"] = {"value": rate, "unit": UNIT, "cores": info["cores"], "kind": "port",
+        result["cpu_baseline"] = {"value": rate, "unit": UNIT, "cores": info["cores"], "kind": "port", "cpu": cpu_model(),
                                   "sample": info["sample"]}
     if world == 1 and not args.no_extras:
         del state, scratch
