@@ -5,7 +5,8 @@
   rolled half step, BIT FOR BIT (every cell runs the same arithmetic wherever its tile sits),
   for the fused and the two-kernel (chunked coefficient field) paths and both gather offsets;
 * linearity -- step(a u + b v) = a step(u) + b step(v) to FP64 rounding;
-* fused vs two-kernel agreement to 1e-12 (same exact operator, different factorisation).
+* fused vs two-kernel agreement to 1e-12 (same exact operator, different factorisation);
+* the same shift / linearity properties for m = 5 at configs[3]'s 256 x 256 plane.
 """
 
 import numpy as np
@@ -62,3 +63,38 @@ def test_linearity_and_fused_vs_two_kernel_full_plane():
     assert rm.rel_err(sw.cpu().numpy(), lin.cpu().numpy()) <= 1e-14
     two = _half(u, hb.StepConfig(mode="two_pass", variant="separable", coeff_budget_bytes=12 << 30), ops, dt)
     assert rm.rel_err(two.cpu().numpy(), su.cpu().numpy()) <= 1e-12
+
+
+CELLS5 = (256, 256, 16)  # configs[3]'s plane (m = 5, 256^3): same tiles and waves per plane
+
+
+@pytest.mark.parametrize("mode", ["fused", "two_pass"])
+@pytest.mark.parametrize("parity", ["primary", "dual"])
+def test_shift_equivariance_bitwise_full_plane_m5(mode, parity):
+    """m = 5 DMMA cell-pair kernels (fused; reconstruction + evolution with a chunked
+    coefficient field) at configs[3]'s plane size: rolled input -> rolled output, bit for bit."""
+    grid = hb.GridSpec(CELLS5)
+    cfg = hb.StepConfig(mode=mode, variant="separable", coeff_budget_bytes=4 << 30)
+    ops = hb.OperatorSet.for_grid(grid, 5)
+    dt = hb.select_dt(grid, cfg)
+    u = _field(4, grid, n=5, parity=parity)
+    out = _half(u, cfg, ops, dt)
+    shift = (3, 7, 5)
+    rolled = hb.DofField(u.grid, 5, torch.roll(u.tensor, shifts=shift, dims=(0, 1, 2)).contiguous())
+    del u
+    out_r = _half(rolled, cfg, ops, dt)
+    assert torch.equal(out_r, torch.roll(out, shifts=shift, dims=(0, 1, 2)))
+
+
+def test_linearity_full_plane_m5():
+    grid = hb.GridSpec(CELLS5)
+    ops = hb.OperatorSet.for_grid(grid, 5)
+    cfg = hb.StepConfig(variant="separable")
+    dt = hb.select_dt(grid, cfg)
+    u, v = _field(5, grid, n=5), _field(6, grid, n=5)
+    a, b = -0.5, 2.0
+    su, sv = _half(u, cfg, ops, dt), _half(v, cfg, ops, dt)
+    sw = _half(hb.DofField(u.grid, 5, a * u.tensor + b * v.tensor), cfg, ops, dt)
+    # one DMMA contraction chain per output; the operators' growth (max|A| ~ 1e2 at N = 5) sets
+    # the rounding scale
+    assert rm.rel_err(sw.cpu().numpy(), (a * su + b * sv).cpu().numpy()) <= 1e-13
