@@ -433,7 +433,9 @@ recon_dmma_cp_kernel(const double* __restrict__ src, double* __restrict__ coeff,
         const int cell = lc / S2, r = lc - cell * S2;
         const int cx = cx0 + cell % TX, cy = cy0 + cell / C::TX;
         r3[it] = cell * VCS + r;
-        o3[it] = (l < L3 && cx < M1 && cy < M2) ? (cy * M1 + cx) * S3 + (2 * q) * S2 + r : -1;  // + 8 cb S2
+        // relative to the tile's first cell (int32 up to M1 < 2^31 / (TY S^3)): the coefficient
+        // plane itself (M1 M2 S^3 doubles) may exceed 2^31 elements
+        o3[it] = (l < L3 && cx < M1 && cy < M2) ? ((cy - cy0) * M1 + (cx - cx0)) * S3 + (2 * q) * S2 + r : -1;  // + 8 cb S2
     }
 
     // x3 of cell plane p-2 shares a barrier interval with x1 of node plane p (2 barriers per plane)
@@ -451,7 +453,7 @@ recon_dmma_cp_kernel(const double* __restrict__ src, double* __restrict__ coeff,
             const double* vk[KS];
 #pragma unroll
             for (int ks = 0; ks < KS; ++ks) vk[ks] = V + ((cp + ka[ks]) & 1) * C::V_D + k3[ks];
-            double* oplane = coeff + (zc0 - d.z_begin + cp) * cplane;
+            double* oplane = coeff + (zc0 - d.z_begin + cp) * cplane + ((int64_t)cy0 * M1 + cx0) * S3;
 #pragma unroll
             for (int it = 0; it < I3; ++it) {
                 if (!live<C::G3, WARPS>(warp, it)) continue;  // warp-uniform: no dummy DMMAs
@@ -521,7 +523,8 @@ int recon_dmma5_launch(const double* src, double* coeff, const Dims& d, const do
     using C = rcp::Cfg<5, 4, 2, 2>;
     const int64_t nz = d.z_end - d.z_begin;
     if (nz <= 0) return 0;
-    if (d.M1 * d.M2 * C::S3 >= (int64_t(1) << 31)) return (int)cudaErrorInvalidValue;  // int32 plane offsets
+    if (d.M1 * d.M2 * C::n3 >= (int64_t(1) << 31) || d.M1 * C::TY * C::S3 >= (int64_t(1) << 31))
+        return (int)cudaErrorInvalidValue;  // int32 node-plane / tile-relative output offsets
     LitOps<double, 5> hp;
     for (int i = 0; i < C::S2; ++i) hp.H[i] = h_mat[i];
     for (int i = 0; i < C::S; ++i) hp.f1[i] = hp.f2[i] = hp.f3[i] = 0.0;

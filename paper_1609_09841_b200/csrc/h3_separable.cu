@@ -444,7 +444,6 @@ static int sep_evolve_n(const double* coeff, double* dst, const Dims& d, const d
         if (cpb == 2) return sep_evolve_nc<3, 2>(coeff, dst, d, Sh, st, first_bad, guard);
         if (cpb == 42) return sep_evolve_nc<3, 4, 2>(coeff, dst, d, Sh, st, first_bad, guard);
         if (cpb == 8) return sep_evolve_nc<3, 8>(coeff, dst, d, Sh, st, first_bad, guard);
-        if (cpb == 8) return sep_evolve_nc<3, 8>(coeff, dst, d, Sh, st, first_bad, guard);
         // one cell (64 threads) per CTA: 32 independent CTAs per SM overlap their load and
         // contraction phases best (measured 4.7 vs 4.2 TB/s for 2-8 cells per CTA)
         return sep_evolve_nc<3, 1>(coeff, dst, d, Sh, st, first_bad, guard);
