@@ -349,6 +349,8 @@ def main():
                      "algorithmic_bytes_per_launch": alg_bytes, "mean_launch_ms": launch_ms,
                      "peak_source": peak_src},
         "gpu_launches": launches_per_step * args.steps,
+        # also the per-half-step node rate (nodes updated per second, whole job)
+        "node_updates_per_s_per_half_step": (dofs_per_step // n3) / (ms_max / args.steps / 2 / 1e3),
         "finite": finite,
     }
     result["clocks"] = clocks.summary()
