@@ -53,6 +53,25 @@ def test_select_dt_and_factor_arrays_match_oracle():
         assert a.dtype == b.dtype and np.array_equal(a, b)
 
 
+@pytest.mark.parametrize("order_n", range(9))
+def test_interp_matrix_inverts_the_endpoint_vandermonde_exactly(order_n):
+    """H (built from closed-form Hermite cardinal polynomials) is the exact inverse of the
+    reference's defining matrix V[(e,k)][j] = C(j,k) z_e^(j-k), z_e = -/+ 1/2."""
+    import math
+    from fractions import Fraction
+    from paper_1609_09841_b200.operators import interp_matrix_rational
+    side, n = 2 * order_n + 2, order_n + 1
+    V = [[Fraction(0)] * side for _ in range(side)]
+    for e, z in enumerate((Fraction(-1, 2), Fraction(1, 2))):
+        for k in range(n):
+            for j in range(k, side):
+                V[e * n + k][j] = math.comb(j, k) * z ** (j - k)
+    H = interp_matrix_rational(order_n)
+    for r in range(side):
+        for c in range(side):
+            assert sum(V[r][j] * H[j][c] for j in range(side)) == (1 if r == c else 0)
+
+
 @pytest.mark.parametrize("order_n", range(7))
 def test_interp_matrix_bit_identical_to_reference(order_n):
     expected = np.array([[float.fromhex(v) for v in row] for row in GOLDEN["interp_matrix_hex"][str(order_n)]])
