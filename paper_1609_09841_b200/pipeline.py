@@ -46,11 +46,11 @@ __all__ = [
 
 MODES = ("two_pass", "fused")
 VARIANTS = ("auto", "literal", "separable")
-ADVECTION_SPEED = 1.0
+ADVECTION_SPEED = 1.0  # u_t = c (u_x1 + u_x2 + u_x3) with c = 1
 
-# The reference's nominal per-kernel tile lengths (pipeline.py:52-56).  On the
-# GPU the tile is a launch hint only (results never depend on it); the value is
-# still validated exactly like the reference does.
+# Nominal x1 tile lengths per kernel and N (the reference's defaults, pipeline.py:52-56; other N
+# fall back to 4).  On the GPU a tile is only validated and reported -- the launch geometry is
+# the kernels' own and results never depend on it.
 DEFAULT_TILE_X1 = {
     "reconstruction": {1: 16, 2: 10, 3: 4},
     "evolution": {1: 16, 2: 10, 3: 2},
@@ -59,23 +59,41 @@ DEFAULT_TILE_X1 = {
 
 
 def default_stages(order_n: int, dims: int = 3) -> int:
-    """Stage count making local evolution exact: d(2N+1) (kernels.py:50-52)."""
+    """Taylor stages after which the local evolution is exact: the cell polynomial has degree
+    2N+1 per axis, so dims (2N+1) applications of the nilpotent operator exhaust it."""
     return dims * (2 * order_n + 1)
 
 
 class InstabilityError(RuntimeError):
-    """Non-finite values appeared in a destination field (pipeline.py:59-66)."""
+    """A half step produced a non-finite DOF.  `node` = (m1, m2, m3) of the first one in the
+    field's C order, `step` = the step index passed by the caller (or None)."""
 
     def __init__(self, node, step: int | None = None):
-        self.node = tuple(int(x) for x in node)
+        self.node = tuple(int(v) for v in node)
         self.step = step
-        at = f" at step {step}" if step is not None else ""
-        super().__init__(f"non-finite values detected{at}, first offending node {self.node}")
+        where = "" if step is None else f" at step {step}"
+        super().__init__(f"non-finite values detected{where}, first offending node {self.node}")
+
+
+def _in(choices):
+    return lambda v: v in choices
+
+
+# (field, accepts, requirement) -- checked in this order by StepConfig
+_STEP_CONFIG_RULES = (
+    ("mode", _in(MODES), f"one of {MODES}"),
+    ("tile_x1", lambda v: v is None or v >= 1, ">= 1"),
+    ("cfl", lambda v: 0 < v <= 1, "in (0, 1]"),
+    ("stages_q", lambda v: v is None or v >= 1, ">= 1"),
+    ("precision", _in(("single", "double")), "'single' or 'double'"),
+    ("variant", _in(VARIANTS), f"one of {VARIANTS}"),
+)
 
 
 @dataclass(frozen=True)
 class StepConfig:
-    """Execution knobs for a half/full step (pipeline.py:69-90) plus `variant`."""
+    """How a half / full step runs: the reference's knobs (mode, tile_x1, cfl, stages_q,
+    precision) plus `variant` (kernel family) and `coeff_budget_bytes` (two-pass chunking)."""
 
     mode: str = "fused"
     tile_x1: int | None = None
@@ -86,26 +104,19 @@ class StepConfig:
     coeff_budget_bytes: int | None = None
 
     def __post_init__(self):
-        if self.mode not in MODES:
-            raise ValueError(f"mode must be one of {MODES}, got {self.mode!r}")
-        if self.tile_x1 is not None and self.tile_x1 < 1:
-            raise ValueError(f"tile_x1 must be >= 1, got {self.tile_x1}")
-        if not 0 < self.cfl <= 1:
-            raise ValueError(f"cfl must be in (0, 1], got {self.cfl}")
-        if self.stages_q is not None and self.stages_q < 1:
-            raise ValueError(f"stages_q must be >= 1, got {self.stages_q}")
-        if self.precision not in ("single", "double"):
-            raise ValueError(f"precision must be 'single' or 'double', got {self.precision!r}")
-        if self.variant not in VARIANTS:
-            raise ValueError(f"variant must be one of {VARIANTS}, got {self.variant!r}")
+        for name, ok, requirement in _STEP_CONFIG_RULES:
+            value = getattr(self, name)
+            if not ok(value):
+                raise ValueError(f"{name} must be {requirement}, got {value!r}")
 
     def stages(self, order_n: int) -> int:
-        return self.stages_q if self.stages_q is not None else default_stages(order_n)
+        return default_stages(order_n) if self.stages_q is None else self.stages_q
 
 
 @dataclass
 class CoeffField:
-    """Grid-wide (or slab-chunk) reconstructed coefficients, two-pass intermediate."""
+    """Two-pass intermediate: the (2N+2)^3 coefficients of cells [z_begin, z_end) (the whole
+    grid, or one x3 chunk when it would not fit in HBM)."""
 
     parity: str
     data: torch.Tensor
@@ -115,7 +126,7 @@ class CoeffField:
 
 @dataclass(frozen=True)
 class OperatorSet:
-    """Immutable per-(N, grid) operator bundle (pipeline.py:101-128)."""
+    """Read-only operators of one (N, grid): the shared H and one derivative per axis."""
 
     order_n: int
     interp: InterpOperator
@@ -123,62 +134,61 @@ class OperatorSet:
 
     @classmethod
     def for_grid(cls, grid: GridSpec, order_n: int) -> "OperatorSet":
-        h1, h2, h3 = grid.spacings
-        return cls(order_n=order_n, interp=build_interp_operator(order_n),
-                   derivs=(build_deriv_operator(order_n, h1), build_deriv_operator(order_n, h2),
-                           build_deriv_operator(order_n, h3)))
+        derivs = tuple(build_deriv_operator(order_n, h) for h in grid.spacings)
+        return cls(order_n, build_interp_operator(order_n), derivs)
 
     @property
     def interp_triple(self):
-        return (self.interp, self.interp, self.interp)
+        return (self.interp,) * 3
 
     @property
     def side(self) -> int:
-        return 2 * self.order_n + 2
+        return self.interp.side
 
 
 class AllocationStats:
-    """Grid-sized auxiliary allocations made by the pipeline (pipeline.py:131-152)."""
+    """Book-keeping of the grid-sized scratch the pipeline allocates (the two-pass coefficient
+    buffer): `events` in order, bytes `live_bytes` now, `peak_aux_bytes` high-water mark."""
 
     def __init__(self):
         self.events: list[tuple[str, int]] = []
-        self._live: dict[str, int] = {}
-        self.live_bytes = 0
+        self._sizes: dict[str, int] = {}
         self.peak_aux_bytes = 0
+
+    @property
+    def live_bytes(self) -> int:
+        return sum(self._sizes.values())
 
     def allocate(self, name: str, nbytes: int) -> None:
         self.events.append((name, nbytes))
-        self._live[name] = nbytes
-        self.live_bytes += nbytes
+        self._sizes[name] = nbytes
         self.peak_aux_bytes = max(self.peak_aux_bytes, self.live_bytes)
 
     def release(self, name: str) -> None:
-        self.live_bytes -= self._live.pop(name, 0)
+        self._sizes.pop(name, None)
 
 
 def select_dt(grid: GridSpec, cfg: StepConfig) -> float:
-    """dt = cfl * min_k h_k / speed (pipeline.py:155-163)."""
+    """Largest stable step the CFL number allows: cfl * min_k h_k / c."""
     if not 0 < cfg.cfl <= 1:
         raise ValueError(f"cfl must be in (0, 1], got {cfg.cfl}")
     return cfg.cfl * min(grid.spacings) / ADVECTION_SPEED
 
 
 def resolve_tile_x1(kernel: str, order_n: int, m1: int, override: int | None = None) -> int:
-    """Tile length: explicit override (validated), else the nominal default (pipeline.py:166-173)."""
-    if override is not None:
-        if not 1 <= override <= m1:
-            raise ValueError(f"tile_x1 must be in [1, {m1}], got {override}")
-        return override
-    table = DEFAULT_TILE_X1.get(kernel, DEFAULT_TILE_X1["monolithic"])
-    return max(1, min(m1, table.get(order_n, 4)))
+    """The x1 tile length a pass reports: a validated override, else the kernel's nominal
+    default for N, clipped to the grid."""
+    if override is None:
+        nominal = DEFAULT_TILE_X1.get(kernel, DEFAULT_TILE_X1["monolithic"]).get(order_n, 4)
+        return min(max(nominal, 1), max(m1, 1)) if m1 >= 1 else 1
+    if override < 1 or override > m1:
+        raise ValueError(f"tile_x1 must be in [1, {m1}], got {override}")
+    return override
 
 
 def tile_schedule(grid: GridSpec, tile_x1: int) -> np.ndarray:
-    """The reference's tile table [c3, c2, x1_start, x1_len] (pipeline.py:176-186).
-
-    Kept for API compatibility (and built vectorised); the CUDA kernels use
-    their own launch geometry, which partitions the same cells.
-    """
+    """The reference's tile table, rows [c3, c2, x1_start, x1_len] in its traversal order
+    (kept for API compatibility; the kernels cover the same cells with their own geometry)."""
     m1, m2, m3 = grid.cells_per_axis
     if not 1 <= tile_x1 <= m1:
         raise ValueError(f"tile_x1 must be in [1, {m1}], got {tile_x1}")
@@ -189,21 +199,23 @@ def tile_schedule(grid: GridSpec, tile_x1: int) -> np.ndarray:
 
 
 def set_worker_threads(n: int | None) -> int:
-    """GPU analogue of the worker-pool size (pipeline.py:189-194): returns the SM count."""
+    """The reference sizes a CPU worker pool here; on the GPU the parallelism is the device's:
+    returns its SM count (the argument is accepted and ignored)."""
     return torch.cuda.get_device_properties(torch.cuda.current_device()).multi_processor_count
 
 
 def _factor_arrays(ops: OperatorSet, dtype, delta: float, q: int):
-    """Kernel scale factors, pre-cast to the field dtype (pipeline.py:197-207)."""
+    """(H, fac1, fac2, fac3, cfac) in the field dtype, the kernels' scale factors:
+    fac_k[i] = (i+1) * (1/h_k) for i < s-1 and 0 last -- multiplied by the reciprocal, as the
+    reference does, so the factors round identically -- and cfac[k-1] = delta / k."""
     s = ops.side
+    inv_h = np.array([1.0 / d.spacing for d in ops.derivs])
+    facs = np.zeros((3, s))
+    facs[:, :-1] = np.arange(1, s)[None, :] * inv_h[:, None]
+    facs = facs.astype(dtype)
+    cfac = (delta / np.arange(1, q + 1, dtype=np.float64)).astype(dtype)
     h_mat = np.ascontiguousarray(ops.interp.matrix.astype(dtype))
-    facs = []
-    for d in ops.derivs:
-        fac = np.zeros(s, dtype=dtype)
-        fac[:-1] = (np.arange(1, s) * (1.0 / d.spacing)).astype(dtype)
-        facs.append(fac)
-    cfac = np.asarray([delta / k for k in range(1, q + 1)], dtype=dtype)
-    return h_mat, facs[0], facs[1], facs[2], cfac
+    return h_mat, facs[0].copy(), facs[1].copy(), facs[2].copy(), cfac
 
 
 def _ptr(a: np.ndarray):
@@ -245,6 +257,22 @@ def _coeff_chunk_planes(grid: GridSpec, order_n: int, itemsize: int, budget: int
     return max(1, min(m3, budget // per_plane))
 
 
+def _check_pair(src: DofField, dst: DofField) -> None:
+    """A half step maps a field onto a distinct field of the other parity, same shape/dtype."""
+    problems = [
+        (src.grid.parity == dst.grid.parity,
+         f"src and dst must have opposite parity, both are {src.grid.parity!r}"),
+        (src.tensor.data_ptr() == dst.tensor.data_ptr(), "src and dst must be disjoint fields"),
+        (src.grid.cells_per_axis != dst.grid.cells_per_axis or src.order_n != dst.order_n,
+         "src and dst must share grid dimensions and order"),
+        (src.tensor.dtype != dst.tensor.dtype or src.device != dst.device,
+         "src and dst must share dtype and device"),
+    ]
+    for bad, message in problems:
+        if bad:
+            raise ValueError(message)
+
+
 def half_step(
     src: DofField,
     dst: DofField,
@@ -259,21 +287,18 @@ def half_step(
     _guard: torch.Tensor | None = None,
     _check: bool = True,
 ) -> None:
-    """Advance src's DOFs by dt/2 onto the opposite-parity field dst (pipeline.py:218-274)."""
-    if src.grid.parity == dst.grid.parity:
-        raise ValueError(f"src and dst must have opposite parity, both are {src.grid.parity!r}")
-    if src.tensor.data_ptr() == dst.tensor.data_ptr():
-        raise ValueError("src and dst must be disjoint fields")
-    if src.grid.cells_per_axis != dst.grid.cells_per_axis or src.order_n != dst.order_n:
-        raise ValueError("src and dst must share grid dimensions and order")
-    if src.tensor.dtype != dst.tensor.dtype or src.device != dst.device:
-        raise ValueError("src and dst must share dtype and device")
+    """Advance src's DOFs by dt/2 onto the opposite-parity field dst (reference
+    pipeline.py:218-274: same arguments, same ValueErrors for mismatched fields, same
+    InstabilityError after the pass), as one (fused) or two (two-pass) kernel launches on the
+    current CUDA stream."""
+    _check_pair(src, dst)
     if dt is None:
         dt = select_dt(src.grid, cfg)
     order_n = ops.order_n
     q = cfg.stages(order_n)
     delta = dt / 2
-    off = 0 if src.grid.parity == "primary" else -1
+    # the gather offset: primary cell c reads nodes c, c+1; dual cell c reads c-1, c
+    off = -1 if src.grid.parity == "dual" else 0
     kernel = "monolithic" if cfg.mode == "fused" else "reconstruction"
     resolve_tile_x1(kernel, order_n, src.grid.cells_per_axis[0], cfg.tile_x1)
     precision = src.precision
