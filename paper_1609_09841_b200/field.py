@@ -28,22 +28,25 @@ __all__ = ["GridSpec", "DofField", "write_snapshot", "read_snapshot", "PRECISION
 PARITIES = ("primary", "dual")
 PRECISION_DTYPES = {"single": np.float32, "double": np.float64}
 _TORCH_DTYPES = {"single": torch.float32, "double": torch.float64}
+_SNAPSHOT_LAYOUT = "m3,m2,m1,n3,n2,n1"
 
 
 @dataclass(frozen=True)
 class GridSpec:
-    """Periodic tensor grid: M_k cells and domain length L_k per axis (field.py:34-77)."""
+    """Periodic tensor-product grid: `cells_per_axis` (M1, M2, M3) over `domain_lengths`
+    (L1, L2, L3); primary nodes sit at m h, dual nodes at (m + 1/2) h (reference field.py:34-77)."""
 
     cells_per_axis: tuple[int, int, int]
     domain_lengths: tuple[float, float, float] = (1.0, 1.0, 1.0)
     parity: str = "primary"
 
     def __post_init__(self):
-        cells = tuple(self.cells_per_axis)
-        lengths = tuple(self.domain_lengths)
-        if len(cells) != 3 or any(int(m) != m or m < 1 for m in cells):
+        cells, lengths = tuple(self.cells_per_axis), tuple(self.domain_lengths)
+        cells_ok = len(cells) == 3 and all(int(m) == m and m >= 1 for m in cells)
+        lengths_ok = len(lengths) == 3 and all(l > 0 for l in lengths)  # NaN fails too
+        if not cells_ok:
             raise ValueError(f"cells_per_axis must be three positive ints, got {self.cells_per_axis}")
-        if len(lengths) != 3 or any(not (l > 0) for l in lengths):
+        if not lengths_ok:
             raise ValueError(f"domain_lengths must be three positive reals, got {self.domain_lengths}")
         if self.parity not in PARITIES:
             raise ValueError(f"parity must be one of {PARITIES}, got {self.parity!r}")
@@ -51,25 +54,28 @@ class GridSpec:
         object.__setattr__(self, "domain_lengths", lengths)
 
     @property
+    def _shift(self) -> float:
+        return 0.5 if self.parity == "dual" else 0.0
+
+    @property
     def spacings(self) -> tuple[float, float, float]:
-        return tuple(l / m for l, m in zip(self.domain_lengths, self.cells_per_axis))
+        """h_k = L_k / M_k."""
+        return tuple(length / cells for length, cells in zip(self.domain_lengths, self.cells_per_axis))
 
     @property
     def num_cells(self) -> int:
-        m1, m2, m3 = self.cells_per_axis
-        return m1 * m2 * m3
+        return int(np.prod(self.cells_per_axis, dtype=np.int64))
 
     def wrap(self, axis: int, m: int) -> int:
+        """Periodic index along `axis` (1-based, as the reference numbers axes)."""
         return m % self.cells_per_axis[axis - 1]
 
     def node_coord(self, axis: int, m: int) -> float:
-        h = self.spacings[axis - 1]
-        return (self.wrap(axis, m) + (0.5 if self.parity == "dual" else 0.0)) * h
+        return (self.wrap(axis, m) + self._shift) * self.spacings[axis - 1]
 
     def axis_coords(self, axis: int) -> np.ndarray:
-        m = self.cells_per_axis[axis - 1]
-        h = self.spacings[axis - 1]
-        return (np.arange(m) + (0.5 if self.parity == "dual" else 0.0)) * h
+        """Coordinates of this parity's nodes along `axis`, index order."""
+        return (np.arange(self.cells_per_axis[axis - 1]) + self._shift) * self.spacings[axis - 1]
 
     def with_parity(self, parity: str) -> "GridSpec":
         return GridSpec(self.cells_per_axis, self.domain_lengths, parity)
@@ -81,73 +87,68 @@ def _default_device():
     return torch.device("cuda", torch.cuda.current_device())
 
 
-class DofField:
-    """Scaled-derivative DOFs of one parity, resident on the GPU (field.py:80-117).
+def _dof_shape(grid: GridSpec, order_n: int) -> tuple[int, ...]:
+    m1, m2, m3 = grid.cells_per_axis
+    return (m3, m2, m1) + (order_n + 1,) * 3
 
-    `data` may be a numpy array (uploaded) or a CUDA torch tensor (adopted
-    without a copy) of shape (M3, M2, M1, N+1, N+1, N+1).
+
+class DofField:
+    """Scaled-derivative DOFs h^|n|/n! D^n u of one parity, resident in HBM as `.tensor`
+    with the reference's rank-6 layout [m3][m2][m1][n3][n2][n1] (reference field.py:80-117).
+
+    `data` is a numpy array (uploaded) or a torch tensor (a CUDA tensor is adopted without a
+    copy) of shape (M3, M2, M1, N+1, N+1, N+1), float32 or float64.
     """
 
     def __init__(self, grid: GridSpec, order_n: int, data, device=None):
         self.grid = grid
         self.order_n = int(order_n)
-        m1, m2, m3 = grid.cells_per_axis
-        npts = self.order_n + 1
-        expected = (m3, m2, m1, npts, npts, npts)
-        if tuple(data.shape) != expected:
-            raise ValueError(f"data shape {tuple(data.shape)} does not match grid/order {expected}")
-        if isinstance(data, torch.Tensor):
-            if not data.is_cuda:
-                data = data.to(device or _default_device())
-            if data.dtype not in (torch.float32, torch.float64):
-                raise ValueError(f"unsupported dtype {data.dtype}")
-            self.tensor = data.contiguous()
-        else:
-            arr = np.ascontiguousarray(data)
-            if arr.dtype not in (np.float32, np.float64):
-                raise ValueError(f"unsupported dtype {arr.dtype}")
-            self.tensor = torch.from_numpy(arr).to(device or _default_device())
+        want = _dof_shape(grid, self.order_n)
+        if tuple(data.shape) != want:
+            raise ValueError(f"data shape {tuple(data.shape)} does not match grid/order {want}")
+        if not isinstance(data, torch.Tensor):
+            data = torch.from_numpy(np.ascontiguousarray(data))
+        if data.dtype not in (torch.float32, torch.float64):
+            raise ValueError(f"unsupported dtype {data.dtype}")
+        self.tensor = (data if data.is_cuda else data.to(device or _default_device())).contiguous()
+
+    @classmethod
+    def _allocate(cls, fill, grid, order_n, precision, device):
+        if precision not in _TORCH_DTYPES:
+            raise ValueError(f"precision must be one of {tuple(_TORCH_DTYPES)}, got {precision!r}")
+        t = fill(_dof_shape(grid, order_n), dtype=_TORCH_DTYPES[precision], device=device or _default_device())
+        return cls(grid, order_n, t)
 
     @classmethod
     def zeros(cls, grid: GridSpec, order_n: int, precision: str = "double", device=None) -> "DofField":
-        if precision not in PRECISION_DTYPES:
-            raise ValueError(f"precision must be one of {tuple(PRECISION_DTYPES)}, got {precision!r}")
-        m1, m2, m3 = grid.cells_per_axis
-        npts = order_n + 1
-        t = torch.zeros((m3, m2, m1, npts, npts, npts), dtype=_TORCH_DTYPES[precision],
-                        device=device or _default_device())
-        return cls(grid, order_n, t)
+        return cls._allocate(torch.zeros, grid, order_n, precision, device)
 
     @classmethod
     def empty(cls, grid: GridSpec, order_n: int, precision: str = "double", device=None) -> "DofField":
-        """Uninitialised device field (every node is overwritten by a half step)."""
-        m1, m2, m3 = grid.cells_per_axis
-        npts = order_n + 1
-        t = torch.empty((m3, m2, m1, npts, npts, npts), dtype=_TORCH_DTYPES[precision],
-                        device=device or _default_device())
-        return cls(grid, order_n, t)
+        """Uninitialised device field (a half step overwrites every node)."""
+        return cls._allocate(torch.empty, grid, order_n, precision, device)
 
-    # ---- readback ---------------------------------------------------------------------
+    # ---- host readback / upload -------------------------------------------------------------
     @property
     def data(self) -> np.ndarray:
-        """Host copy of the rank-6 DOF tensor (reference layout)."""
+        """Host copy of the DOF tensor in the reference layout."""
         return self.tensor.detach().cpu().numpy()
 
     @data.setter
     def data(self, value) -> None:
-        value = torch.as_tensor(np.ascontiguousarray(value) if not isinstance(value, torch.Tensor) else value)
-        if tuple(value.shape) != tuple(self.tensor.shape):
-            raise ValueError(f"shape {tuple(value.shape)} does not match {tuple(self.tensor.shape)}")
-        self.tensor.copy_(value.to(self.tensor.dtype))
+        src = value if isinstance(value, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(value))
+        if tuple(src.shape) != tuple(self.tensor.shape):
+            raise ValueError(f"shape {tuple(src.shape)} does not match {tuple(self.tensor.shape)}")
+        self.tensor.copy_(src.to(self.tensor.dtype))
 
     @property
     def values(self) -> np.ndarray:
-        """Node values (the n = (0,0,0) DOF), indexed [m3][m2][m1]."""
+        """Point values u at the nodes (DOF index (0, 0, 0)), [m3][m2][m1] on the host."""
         return self.tensor[..., 0, 0, 0].cpu().numpy()
 
     @property
     def precision(self) -> str:
-        return "single" if self.tensor.dtype == torch.float32 else "double"
+        return "double" if self.tensor.dtype == torch.float64 else "single"
 
     @property
     def device(self):
@@ -164,35 +165,33 @@ class DofField:
         return bool(torch.isfinite(self.tensor).all().item())
 
 
-def write_snapshot(field: DofField, base_path, time: float = 0.0) -> tuple[Path, Path]:
-    """<base>.bin (flat little-endian, rank-6 layout) + <base>.json sidecar (field.py:175-201)."""
+def _snapshot_paths(base_path) -> tuple[Path, Path]:
     base = Path(base_path)
-    bin_path, json_path = base.with_suffix(".bin"), base.with_suffix(".json")
+    return base.with_suffix(".bin"), base.with_suffix(".json")
+
+
+def write_snapshot(field: DofField, base_path, time: float = 0.0) -> tuple[Path, Path]:
+    """The reference's snapshot format (field.py:175-201): `<base>.bin` holds the DOFs as flat
+    little-endian floats in the rank-6 layout, `<base>.json` the grid, order, parity,
+    precision, time, layout and dtype."""
+    bin_path, json_path = _snapshot_paths(base_path)
     bin_path.parent.mkdir(parents=True, exist_ok=True)
-    host = field.data
-    bin_path.write_bytes(host.astype(host.dtype.newbyteorder("<"), copy=False).tobytes())
-    meta = {
-        "cells_per_axis": list(field.grid.cells_per_axis),
-        "domain_lengths": list(field.grid.domain_lengths),
-        "order_n": field.order_n,
-        "parity": field.grid.parity,
-        "precision": field.precision,
-        "time": time,
-        "layout": "m3,m2,m1,n3,n2,n1",
-        "dtype": "<f4" if field.precision == "single" else "<f8",
-    }
+    dtype = "<f8" if field.precision == "double" else "<f4"
+    bin_path.write_bytes(np.ascontiguousarray(field.data, dtype=np.dtype(dtype)).tobytes())
+    grid = field.grid
+    meta = dict(cells_per_axis=list(grid.cells_per_axis), domain_lengths=list(grid.domain_lengths),
+                order_n=field.order_n, parity=grid.parity, precision=field.precision, time=time,
+                layout=_SNAPSHOT_LAYOUT, dtype=dtype)
     json_path.write_text(json.dumps(meta, sort_keys=True, indent=2) + "\n")
     return bin_path, json_path
 
 
 def read_snapshot(base_path, device=None) -> tuple[DofField, float]:
-    """Load a snapshot written by write_snapshot (field.py:204-217) onto the GPU."""
-    base = Path(base_path)
-    meta = json.loads(base.with_suffix(".json").read_text())
+    """Load a snapshot (reference field.py:204-217) straight into HBM; returns (field, time)."""
+    bin_path, json_path = _snapshot_paths(base_path)
+    meta = json.loads(json_path.read_text())
     grid = GridSpec(tuple(meta["cells_per_axis"]), tuple(meta["domain_lengths"]), meta["parity"])
     order_n = int(meta["order_n"])
-    npts = order_n + 1
-    m1, m2, m3 = grid.cells_per_axis
-    raw = np.frombuffer(base.with_suffix(".bin").read_bytes(), dtype=np.dtype(meta["dtype"]))
-    data = raw.reshape(m3, m2, m1, npts, npts, npts).astype(PRECISION_DTYPES[meta["precision"]])
-    return DofField(grid, order_n, data, device=device), float(meta["time"])
+    flat = np.frombuffer(bin_path.read_bytes(), dtype=np.dtype(meta["dtype"]))
+    host = flat.reshape(_dof_shape(grid, order_n)).astype(PRECISION_DTYPES[meta["precision"]])
+    return DofField(grid, order_n, host, device=device), float(meta["time"])
