@@ -130,12 +130,14 @@ def build_ic(cfg: RunConfig) -> SeparableIC:
 
 
 def _plan_steps(cfg: RunConfig, grid: GridSpec, step_cfg: StepConfig) -> tuple[int, float]:
-    """Number of full steps and the effective dt (reference runner.py:65-76)."""
-    dt_max = select_dt(grid, step_cfg)
-    if cfg.steps is not None:
-        return cfg.steps, dt_max
-    n = max(1, math.ceil(cfg.final_time / dt_max - 1e-12))
-    return n, cfg.final_time / n
+    """(full steps, dt).  A step count runs at the CFL dt; a final time is reached exactly by
+    the fewest equal steps not exceeding the CFL dt (a 1e-12 slack absorbs T / dt rounding
+    just above an integer) -- the reference runner's plan (runner.py:65-76)."""
+    cfl_dt = select_dt(grid, step_cfg)
+    if cfg.steps is None:
+        count = max(1, math.ceil(cfg.final_time / cfl_dt - 1e-12))
+        return count, cfg.final_time / count
+    return cfg.steps, cfl_dt
 
 
 def _float_cell(x) -> str:
@@ -248,21 +250,25 @@ def execute_converge(cfg: RunConfig, levels: list[int]) -> dict:
     if cfg.final_time is None:
         raise ConfigError("final_time: converge requires final_time (not steps)")
     header = ["cells", "h", "l_inf", "l2", "order_linf", "order_l2"]
-    rows, prev = [], None
+
+    def observed_order(coarse_err, fine_err, refinement):
+        # e ~ C h^p  =>  p = log2(e_coarse / e_fine) / log2(M_fine / M_coarse)
+        return math.log2(coarse_err / fine_err) / refinement if fine_err > 0 else float("inf")
+
+    errors = []  # (M, l_inf, l2) per level
     for m in levels:
         summary = execute_run(replace(cfg, cells=(m, m, m), steps=None), write_artifacts=False)
         if "l_inf" not in summary:
             raise ConfigError("ic: converge requires an IC with an exact solution")
-        l_inf, l2 = summary["l_inf"], summary["l2"]
-        h = cfg.domain[0] / m
-        if prev is None:
-            order_linf = order_l2 = float("nan")
-        else:
-            ratio = math.log2(m / prev[0])
-            order_linf = math.log2(prev[1] / l_inf) / ratio if l_inf > 0 else float("inf")
-            order_l2 = math.log2(prev[2] / l2) / ratio if l2 > 0 else float("inf")
-        rows.append([m, h, l_inf, l2, order_linf, order_l2])
-        prev = (m, l_inf, l2)
+        errors.append((m, summary["l_inf"], summary["l2"]))
+    rows = []
+    for k, (m, l_inf, l2) in enumerate(errors):
+        orders = [float("nan")] * 2
+        if k:
+            m0, e0_inf, e0_l2 = errors[k - 1]
+            refinement = math.log2(m / m0)
+            orders = [observed_order(e0_inf, l_inf, refinement), observed_order(e0_l2, l2, refinement)]
+        rows.append([m, cfg.domain[0] / m, l_inf, l2, *orders])
     csv_path = Path(cfg.out_dir) / "converge.csv"
     _write_csv(csv_path, header, rows)
     return {"status": "ok", "order_n": cfg.order_n, "rows": [dict(zip(header, r)) for r in rows],
