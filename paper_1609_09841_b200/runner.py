@@ -140,17 +140,42 @@ def _plan_steps(cfg: RunConfig, grid: GridSpec, step_cfg: StepConfig) -> tuple[i
     return cfg.steps, cfl_dt
 
 
-def _float_cell(x) -> str:
-    return repr(float(x)) if isinstance(x, (float, np.floating)) else str(x)
-
-
 def _write_csv(path: Path, header, rows) -> None:
+    """CSV with floats written by repr (round-trip exact, as the reference writes them)."""
     path.parent.mkdir(parents=True, exist_ok=True)
+    cell = lambda v: repr(float(v)) if isinstance(v, (float, np.floating)) else str(v)  # noqa: E731
     with open(path, "w", newline="") as fh:
-        w = csv.writer(fh)
-        w.writerow(header)
-        for row in rows:
-            w.writerow([_float_cell(x) for x in row])
+        csv.writer(fh).writerows([list(header)] + [[cell(v) for v in row] for row in rows])
+
+
+def _write_artifacts(cfg, step_cfg, grid, state, t, error_rows, n_steps, wall) -> dict:
+    """snapshot.bin/json, errors.csv (when errors were tracked), perf.json/csv -- the reference
+    runner's artifact set and names; returns {artifact key: path}."""
+    out_dir = Path(cfg.out_dir)
+    out_dir.mkdir(parents=True, exist_ok=True)
+    paths = dict(zip(("snapshot_bin", "snapshot_json"), write_snapshot(state, out_dir / "snapshot", time=t)))
+    if error_rows is not None:
+        paths["errors_csv"] = out_dir / "errors.csv"
+        _write_csv(paths["errors_csv"], ["step", "time", "l_inf", "l2"], error_rows)
+    # perf report: one row per kernel over the whole run (2 half steps per step) plus the total
+    peaks = perf.DevicePeaks.b200()
+    kernels = ("monolithic",) if cfg.mode == "fused" else ("reconstruction", "evolution")
+    passes = 2 * n_steps
+    rows = []
+    for kern in kernels:
+        flops, nbytes = (c * passes for c in perf.model_counts(kern, cfg.order_n, grid, step_cfg))
+        tile = perf.resolve_tile_x1(kern, cfg.order_n, grid.cells_per_axis[0], cfg.tile_x1)
+        rows.append(perf._profile(kern, cfg.order_n, cfg.mode, tile, flops, nbytes,
+                                  max(wall / len(kernels), 1e-12), peaks,
+                                  perf.algorithmic_bytes(kern, cfg.order_n, grid) * passes))
+    rows.append(perf._profile("solution", cfg.order_n, cfg.mode, rows[0].tile_x1,
+                              sum(r.flops_modeled for r in rows), sum(r.bytes_modeled for r in rows),
+                              max(wall, 1e-12), peaks))
+    report = perf.report_dict(rows, peaks)
+    paths["perf_json"], paths["perf_csv"] = out_dir / "perf.json", out_dir / "perf.csv"
+    paths["perf_json"].write_text(json.dumps(report, sort_keys=True, indent=2) + "\n")
+    _write_csv(paths["perf_csv"], perf.REPORT_COLUMNS, [[r[c] for c in perf.REPORT_COLUMNS] for r in report["runs"]])
+    return {key: str(path) for key, path in paths.items()}
 
 
 def execute_run(cfg: RunConfig, write_artifacts: bool = True) -> dict:
@@ -213,33 +238,8 @@ def execute_run(cfg: RunConfig, write_artifacts: bool = True) -> dict:
         result["l_inf"] = error_rows[-1][2]
         result["l2"] = error_rows[-1][3]
     if write_artifacts:
-        out_dir = Path(cfg.out_dir)
-        out_dir.mkdir(parents=True, exist_ok=True)
-        bin_path, json_path = write_snapshot(state, out_dir / "snapshot", time=t)
-        result["artifacts"]["snapshot_bin"] = str(bin_path)
-        result["artifacts"]["snapshot_json"] = str(json_path)
-        if track:
-            errors_path = out_dir / "errors.csv"
-            _write_csv(errors_path, ["step", "time", "l_inf", "l2"], error_rows)
-            result["artifacts"]["errors_csv"] = str(errors_path)
-        peaks = perf.DevicePeaks.b200()
-        kernels = ["monolithic"] if cfg.mode == "fused" else ["reconstruction", "evolution"]
-        rows, tf, tb = [], 0, 0
-        for kern in kernels:
-            f1_, b1_ = perf.model_counts(kern, cfg.order_n, grid, step_cfg)
-            f_, b_ = f1_ * 2 * n_steps, b1_ * 2 * n_steps
-            tf, tb = tf + f_, tb + b_
-            tile = perf.resolve_tile_x1(kern, cfg.order_n, grid.cells_per_axis[0], cfg.tile_x1)
-            rows.append(perf._profile(kern, cfg.order_n, cfg.mode, tile, f_, b_, max(wall / len(kernels), 1e-12),
-                                      peaks, perf.algorithmic_bytes(kern, cfg.order_n, grid) * 2 * n_steps))
-        rows.append(perf._profile("solution", cfg.order_n, cfg.mode, rows[0].tile_x1, tf, tb, max(wall, 1e-12),
-                                  peaks))
-        report = perf.report_dict(rows, peaks)
-        (out_dir / "perf.json").write_text(json.dumps(report, sort_keys=True, indent=2) + "\n")
-        _write_csv(out_dir / "perf.csv", perf.REPORT_COLUMNS,
-                   [[run[c] for c in perf.REPORT_COLUMNS] for run in report["runs"]])
-        result["artifacts"]["perf_json"] = str(out_dir / "perf.json")
-        result["artifacts"]["perf_csv"] = str(out_dir / "perf.csv")
+        result["artifacts"] = _write_artifacts(cfg, step_cfg, grid, state, t, error_rows if track else None,
+                                               n_steps, wall)
     return result
 
 
