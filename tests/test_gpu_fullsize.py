@@ -117,7 +117,8 @@ def test_m5_two_kernel_coefficient_plane_beyond_2pow31_elements():
     assert rm.rel_err(two.cpu().numpy(), fused.cpu().numpy()) <= 1e-9
 
 
-@pytest.mark.parametrize("order_n,cells,tol", [(3, (128, 128, 32), 1e-11), (5, (64, 64, 16), 2.5e-8)])
+@pytest.mark.parametrize("order_n,cells,tol", [(3, (128, 128, 32), 1e-11), (3, CELLS, 1e-11),
+                                               (5, (64, 64, 16), 2.5e-8)])
 def test_separable_vs_literal_at_scale(order_n, cells, tol):
     """Parity beyond the golden sizes: the literal variant is the reference's arithmetic bit for
     bit (pinned by the golden vectors), so the fast separable path is held to the north-star
