@@ -49,23 +49,46 @@ from .pipeline import InstabilityError, OperatorSet, StepConfig, _factor_arrays,
 __all__ = ["chunk_plan", "HostStepper"]
 
 
-def chunk_plan(m3: int, chunk: int) -> list[tuple[int, int]]:
-    """x3 chunks [z0, z1) covering 0..m3, each at least 2 planes (the ghost logic needs it)."""
+def chunk_plan(m3: int, chunk: int, ramp: bool = False) -> list[tuple[int, int]]:
+    """x3 chunks [z0, z1) covering 0..m3, each at least 2 planes (the ghost logic needs it).
+
+    ramp: start and end with small chunks (chunk/8, /4, /2, then full ones, mirrored at the
+    end), so the pipeline's fill (first upload, nothing to download yet) and drain (last
+    downloads, nothing left to upload) are short."""
     if m3 < 2:
         raise ValueError("streaming needs at least two x3 planes")
     chunk = max(2, min(int(chunk), m3))
-    bounds = [(z, min(m3, z + chunk)) for z in range(0, m3, chunk)]
-    if len(bounds) > 1 and bounds[-1][1] - bounds[-1][0] < 2:  # fold a 1-plane tail into its neighbour
-        z0, _ = bounds[-2]
-        bounds[-2:] = [(z0, m3)]
-    return bounds
+    sizes = []
+    if ramp:
+        head = [max(2, chunk >> s) for s in (3, 2, 1)]
+        if 2 * sum(head) < m3:
+            sizes = head
+            tail = head[::-1]
+            left = m3 - 2 * sum(head)
+            sizes += [chunk] * (left // chunk) + ([left % chunk] if left % chunk else []) + tail
+    if not sizes:
+        sizes = [chunk] * (m3 // chunk) + ([m3 % chunk] if m3 % chunk else [])
+    bounds, z = [], 0
+    for size in sizes:
+        bounds.append((z, z + size))
+        z += size
+    # fold chunks of fewer than 2 planes into their predecessor
+    merged = []
+    for z0, z1 in bounds:
+        if merged and z1 - z0 < 2:
+            merged[-1] = (merged[-1][0], z1)
+        else:
+            merged.append((z0, z1))
+    if len(merged) > 1 and merged[0][1] - merged[0][0] < 2:
+        merged[:2] = [(0, merged[1][1])]
+    return merged
 
 
 class HostStepper:
     """Streamed full steps of a pinned host field (M3, M2, M1, n, n, n), updated in place."""
 
     def __init__(self, host_state: torch.Tensor, grid: GridSpec, order_n: int, cfg: StepConfig | None = None,
-                 chunk_planes: int | None = None, device=None, group=None):
+                 chunk_planes: int | None = None, device=None, group=None, ramp: bool = True):
         """`grid` is the global grid.  Without a multi-rank process group `host_state` is the
         whole field (M3, M2, M1, n, n, n); with one (`group`, default: the default group when
         torch.distributed is initialised) it is this rank's slab (z1 - z0, M2, M1, n, n, n),
@@ -98,7 +121,7 @@ class HostStepper:
         plane = m1 * m2 * n ** 3
         if chunk_planes is None:  # ~2 GB chunks: measured best at 512^3 (tools/time_stream.py)
             chunk_planes = max(2, (2 << 30) // (plane * 8))
-        self.chunks = chunk_plan(planes, chunk_planes)
+        self.chunks = chunk_plan(planes, chunk_planes, ramp=ramp)
         cmax = max(z1 - z0 for z0, z1 in self.chunks)
         kw = dict(dtype=torch.float64, device=self.device)
         shape = lambda planes: (planes, m2, m1, n, n, n)  # noqa: E731

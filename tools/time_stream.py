@@ -37,15 +37,16 @@ print(f"H2D+D2H concurrent {2 * nbytes / (time.perf_counter() - t0) / 1e9:.1f} G
 del dev, dev2
 torch.cuda.empty_cache()
 plane = m * m * (n + 1) ** 3 * 8
-for planes in [int(a) for a in (sys.argv[2].split(",") if len(sys.argv) > 2 else ["8", "16", "32", "64"])]:
-    stp = hb.HostStepper(host, grid, n, cfg, chunk_planes=planes)
+for arg in (sys.argv[2].split(",") if len(sys.argv) > 2 else ["8", "16", "32", "64"]):
+    planes, ramp = int(arg.rstrip("r")), arg.endswith("r")  # "16r": ramped chunk sizes
+    stp = hb.HostStepper(host, grid, n, cfg, chunk_planes=planes, ramp=ramp)
     stp.step()
     torch.cuda.synchronize()
     t0 = time.perf_counter()
     for k in range(2):
         stp.step(step_index=k)
     dt = (time.perf_counter() - t0) / 2
-    print(f"chunk {planes} planes ({planes * plane / 1e9:.1f} GB, {len(stp.chunks)} chunks): {dt:.3f} s/step, "
+    print(f"chunk {planes}{'r' if ramp else ''} planes ({planes * plane / 1e9:.1f} GB, {len(stp.chunks)} chunks): {dt:.3f} s/step, "
           f"{m ** 3 * (n + 1) ** 3 / dt:.3e} DOF-updates/s, {(stp.h2d_bytes + stp.d2h_bytes) / dt / 1e9:.1f} GB/s PCIe", flush=True)
     del stp
     torch.cuda.empty_cache()
