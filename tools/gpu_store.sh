@@ -1,4 +1,6 @@
 # output-store cache policy of the N=3 fused kernel: .cs (default) vs write-back vs L1::no_allocate
+# (needs paper_1609_09841_b200/libh3b200_v1.so / _v2.so built with -DH3_OUT_STORE=1 / 2 of the
+#  out_store() helper used for this measurement; the shipped kernel keeps st.global.cs)
 cd $GRAFT_REPO_ROOT; mkdir -p gpurun_out
 L=paper_1609_09841_b200/libh3b200.so
 cp $L /tmp/v0.so
