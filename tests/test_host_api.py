@@ -161,6 +161,36 @@ def test_abi_argument_validation_without_gpu():
     assert _native.error_string(-2).startswith("order_n")
 
 
+def test_halo_abi_argument_validation_without_gpu():
+    """h3_fused_pass_halo (the multi-GPU slab entry) rejects bad arguments before touching the
+    device: orders without a ghost-pointer kernel, the literal variant, a missing ghost plane
+    the slab needs, bad offsets and inexact stage counts; IPC helpers reject null arguments."""
+    so = _native.lib()
+    dummy = ctypes.c_void_p(16)
+    arr = np.zeros(256)
+    p = arr.ctypes.data_as(ctypes.c_void_p)
+    keys = ["src", "dst", "M1", "M2", "M3", "N", "h", "f1", "f2", "f3", "cf", "q", "off", "zb", "ze",
+            "glo", "ghi", "var", "st", "fb", "g"]
+    base = dict(src=dummy, dst=dummy, M1=4, M2=4, M3=4, N=3, h=p, f1=p, f2=p, f3=p, cf=p, q=21, off=0,
+                zb=0, ze=4, glo=dummy, ghi=dummy, var=2, st=None, fb=None, g=None)
+
+    def call(**over):
+        args = dict(base, **over)
+        return so.h3_fused_pass_halo(*[args[k] for k in keys])
+
+    assert call(N=2, q=15) == -4 and call(var=1) == -4      # no ghost-pointer kernel / literal
+    assert call(ghi=None) == -1                               # off = 0 needs plane M3 of the slab
+    assert call(off=-1, glo=None) == -1                       # off = -1 needs plane -1
+    assert call(off=1) == -1 and call(src=None) == -1
+    assert call(q=20) == -3                                   # separable needs q >= 3(2N+1) = 21
+    assert call(zb=3, ze=2) == -1
+    h = (ctypes.c_ubyte * 64)()
+    off = ctypes.c_int64()
+    assert so.h3_ipc_export(None, h, ctypes.byref(off)) == -1
+    assert so.h3_ipc_open(None, ctypes.byref(ctypes.c_void_p())) == -1
+    assert so.h3_ipc_close(None) == -1
+
+
 @pytest.mark.parametrize("order_n", [0, 1, 3, 5])
 def test_separable_operators_exact(order_n):
     """h3_separable_operators (host math of the fast path) against exact rationals."""
