@@ -1,6 +1,7 @@
 """Run orchestration on the B200: the reference runner's stepping loop, with the GPU kept busy.
 
-Mirror of `execute_run` / `execute_converge` (reference pkg/src/hermite3d/runner.py:135-230)
+Mirror of `execute_run` / `execute_converge` / `execute_bench` (reference
+pkg/src/hermite3d/runner.py:135-269)
 for library callers: same step planning (`_plan_steps`, runner.py:65-76), the same artifacts
 (snapshot.bin/json, errors.csv, perf.json/perf.csv) and the same summary keys.  The reference's
 pydantic RunConfig / CLI / REST layers are out of scope; `RunConfig` here is a
@@ -33,7 +34,7 @@ from .pipeline import AllocationStats, InstabilityError, OperatorSet, StepConfig
 from .problems import Constant, FourierMode, Monomial, SeparableIC, error_norms_async, exact_solution, init_field, \
     plane_wave
 
-__all__ = ["RunConfig", "ConfigError", "build_ic", "execute_run", "execute_converge"]
+__all__ = ["RunConfig", "ConfigError", "build_ic", "execute_run", "execute_converge", "execute_bench"]
 
 
 class ConfigError(ValueError):
@@ -159,7 +160,7 @@ def _write_artifacts(cfg, step_cfg, grid, state, t, error_rows, n_steps, wall) -
         _write_csv(paths["errors_csv"], ["step", "time", "l_inf", "l2"], error_rows)
     # perf report: one row per kernel over the whole run (2 half steps per step) plus the total
     peaks = perf.DevicePeaks.b200()
-    kernels = ("monolithic",) if cfg.mode == "fused" else ("reconstruction", "evolution")
+    kernels = _kernels_of(cfg.mode)
     passes = 2 * n_steps
     rows = []
     for kern in kernels:
@@ -168,14 +169,31 @@ def _write_artifacts(cfg, step_cfg, grid, state, t, error_rows, n_steps, wall) -
         rows.append(perf._profile(kern, cfg.order_n, cfg.mode, tile, flops, nbytes,
                                   max(wall / len(kernels), 1e-12), peaks,
                                   perf.algorithmic_bytes(kern, cfg.order_n, grid) * passes))
-    rows.append(perf._profile("solution", cfg.order_n, cfg.mode, rows[0].tile_x1,
-                              sum(r.flops_modeled for r in rows), sum(r.bytes_modeled for r in rows),
-                              max(wall, 1e-12), peaks))
+    rows.append(_solution_row(cfg, grid, step_cfg, cfg.mode, n_steps, wall, peaks))
+    paths.update(_write_perf(out_dir, rows, peaks)[1])
+    return {key: str(path) for key, path in paths.items()}
+
+
+def _kernels_of(mode: str) -> tuple[str, ...]:
+    return ("monolithic",) if mode == "fused" else ("reconstruction", "evolution")
+
+
+def _solution_row(cfg, grid, step_cfg, mode, n_steps, seconds, peaks) -> perf.KernelProfile:
+    """End-to-end row of a run: modelled counts of all its passes against its wall time."""
+    counts = [perf.model_counts(k, cfg.order_n, grid, step_cfg) for k in _kernels_of(mode)]
+    tile = perf.resolve_tile_x1(_kernels_of(mode)[0], cfg.order_n, grid.cells_per_axis[0], cfg.tile_x1)
+    return perf._profile("solution", cfg.order_n, mode, tile, sum(f for f, _ in counts) * 2 * n_steps,
+                         sum(b for _, b in counts) * 2 * n_steps, max(seconds, 1e-12), peaks)
+
+
+def _write_perf(out_dir: Path, rows, peaks) -> tuple[dict, dict]:
+    """perf.json + perf.csv of `rows`; returns (report, {artifact key: path})."""
     report = perf.report_dict(rows, peaks)
-    paths["perf_json"], paths["perf_csv"] = out_dir / "perf.json", out_dir / "perf.csv"
+    paths = {"perf_json": out_dir / "perf.json", "perf_csv": out_dir / "perf.csv"}
+    out_dir.mkdir(parents=True, exist_ok=True)
     paths["perf_json"].write_text(json.dumps(report, sort_keys=True, indent=2) + "\n")
     _write_csv(paths["perf_csv"], perf.REPORT_COLUMNS, [[r[c] for c in perf.REPORT_COLUMNS] for r in report["runs"]])
-    return {key: str(path) for key, path in paths.items()}
+    return report, paths
 
 
 def execute_run(cfg: RunConfig, write_artifacts: bool = True) -> dict:
@@ -273,3 +291,25 @@ def execute_converge(cfg: RunConfig, levels: list[int]) -> dict:
     _write_csv(csv_path, header, rows)
     return {"status": "ok", "order_n": cfg.order_n, "rows": [dict(zip(header, r)) for r in rows],
             "artifacts": {"converge_csv": str(csv_path)}}
+
+
+def execute_bench(cfg: RunConfig, repetitions: int = 3, modes: list[str] | None = None) -> dict:
+    """Kernel profiles plus the end-to-end run time per mode (reference runner.py:239-269).
+
+    For each mode: `perf.profile_run` (CUDA-event medians of the mode's kernels on a seeded
+    random field) and one `execute_run` without artifacts, reported as a "solution" row with
+    the modelled counts of all its passes; perf.json / perf.csv go to `cfg.out_dir`.  Peaks are
+    the B200's measured ones (`DevicePeaks.b200()`), as in `execute_run`'s report.
+    """
+    peaks = perf.DevicePeaks.b200()
+    grid = GridSpec(cfg.cells, cfg.domain, "primary")
+    rows = []
+    for mode in modes or [cfg.mode]:
+        mode_cfg = replace(cfg, mode=mode)
+        step_cfg = mode_cfg.step_config()
+        rows += perf.profile_run(step_cfg, grid, cfg.order_n, repetitions=repetitions, peaks=peaks,
+                                 rng_seed=cfg.seed)
+        summary = execute_run(mode_cfg, write_artifacts=False)
+        rows.append(_solution_row(mode_cfg, grid, step_cfg, mode, summary["steps"], summary["seconds"], peaks))
+    report, paths = _write_perf(Path(cfg.out_dir), rows, peaks)
+    return {"status": "ok", "runs": report["runs"], "artifacts": {k: str(v) for k, v in paths.items()}}

@@ -106,3 +106,19 @@ def test_resume_from_snapshot_continues_the_run(tmp_path):
     with pytest.raises(runner.ConfigError, match="resume"):
         runner.execute_run(runner.RunConfig(steps=1, out_dir=str(tmp_path / "c"), resume=snap,
                                             order_n=3, cells=(12, 10, 9)))
+
+
+@pytest.mark.gpu
+@pytest.mark.filterwarnings("ignore:.*launch latency:RuntimeWarning")  # deliberately tiny grid
+def test_execute_bench_profiles_and_solution_rows(tmp_path):
+    """execute_bench (reference runner.py:239-269): per mode the kernel profiles then one
+    end-to-end "solution" row; perf.json / perf.csv written; counts from the reference model."""
+    cfg = runner.RunConfig(order_n=3, cells=(24, 20, 16), steps=3, out_dir=str(tmp_path), variant="separable")
+    out = runner.execute_bench(cfg, repetitions=3, modes=["fused", "two_pass"])
+    kernels = [r["kernel"] for r in out["runs"]]
+    assert kernels == ["monolithic", "solution", "reconstruction", "evolution", "solution"]
+    assert all(r["seconds"] > 0 for r in out["runs"])
+    grid = hb.GridSpec((24, 20, 16))
+    f, b = hb.perf.model_counts("monolithic", 3, grid, cfg.step_config())
+    assert out["runs"][1]["flops"] == f * 2 * 3 and out["runs"][1]["bytes"] == b * 2 * 3
+    assert (tmp_path / "perf.json").exists() and (tmp_path / "perf.csv").exists()
