@@ -29,12 +29,13 @@ import torch
 
 from . import perf
 from .field import DofField, GridSpec, read_snapshot, write_snapshot
-from .pipeline import AllocationStats, InstabilityError, OperatorSet, StepConfig, _new_flags, _node_of, half_step, \
-    select_dt
+from .pipeline import AllocationStats, InstabilityError, OperatorSet, StepConfig, _new_flags, _node_of, full_step, \
+    half_step, select_dt
 from .problems import Constant, FourierMode, Monomial, SeparableIC, error_norms_async, exact_solution, init_field, \
     plane_wave
 
-__all__ = ["RunConfig", "ConfigError", "build_ic", "execute_run", "execute_converge", "execute_bench"]
+__all__ = ["RunConfig", "ConfigError", "build_ic", "execute_run", "execute_converge", "execute_bench",
+           "execute_autotune"]
 
 
 class ConfigError(ValueError):
@@ -313,3 +314,56 @@ def execute_bench(cfg: RunConfig, repetitions: int = 3, modes: list[str] | None 
         rows.append(_solution_row(mode_cfg, grid, step_cfg, mode, summary["steps"], summary["seconds"], peaks))
     report, paths = _write_perf(Path(cfg.out_dir), rows, peaks)
     return {"status": "ok", "runs": report["runs"], "artifacts": {k: str(v) for k, v in paths.items()}}
+
+
+def execute_autotune(cfg: RunConfig, candidates: list[int], repetitions: int = 3) -> dict:
+    """Pick tile_x1 by timing full steps per candidate (reference runner.py:272-327: median of
+    `repetitions` after a warm-up step, argmin wins, ties go to the smaller tile; candidates
+    wider than M1 are reported as skipped; autotune.csv in `cfg.out_dir`).
+
+    On the B200 the tile is validated and reported but does not change the kernels' launch
+    geometry, so the candidates time the same up to noise; the API, the table and the selection
+    rule are kept so callers of the reference's autotune keep working.  Times are CUDA-event
+    medians of one full step.
+    """
+    import statistics
+    if len(candidates) < 2:
+        raise ConfigError("candidates: need at least two tile candidates")
+    grid = GridSpec(cfg.cells, cfg.domain, "primary")
+    ops = OperatorSet.for_grid(grid, cfg.order_n)
+    ic = build_ic(cfg)
+    m1 = cfg.cells[0]
+    gather = "monolithic" if cfg.mode == "fused" else "reconstruction"
+    rows, best = [], None
+    for tile in candidates:
+        if tile > m1:
+            rows.append({"tile_x1": tile, "seconds": None, "bytes_modeled": None,
+                         "status": f"skipped: exceeds M1={m1}"})
+            continue
+        step_cfg = replace(cfg, tile_x1=tile).step_config()
+        state = init_field(ic, grid, cfg.order_n, precision=cfg.precision)
+        scratch = DofField.zeros(grid.with_parity("dual"), cfg.order_n, precision=cfg.precision)
+        dt = select_dt(grid, step_cfg)
+        full_step(state, scratch, step_cfg, ops, dt=dt)  # warm-up
+        times = []
+        for _ in range(repetitions):
+            t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            t0.record()
+            full_step(state, scratch, step_cfg, ops, dt=dt)
+            t1.record()
+            t1.synchronize()
+            times.append(t0.elapsed_time(t1) / 1e3)
+        seconds = statistics.median(times)
+        rows.append({"tile_x1": tile, "seconds": seconds,
+                     "bytes_modeled": perf.model_counts(gather, cfg.order_n, grid, step_cfg)[1], "status": "ok"})
+        best = min(best, (seconds, tile)) if best is not None else (seconds, tile)
+    if best is None:
+        raise ConfigError(f"candidates: no candidate fits M1={m1}")
+    for row in rows:
+        if row["status"] == "ok" and row["tile_x1"] == best[1]:
+            row["status"] = "winner"
+    csv_path = Path(cfg.out_dir) / "autotune.csv"
+    _write_csv(csv_path, ["tile_x1", "seconds", "bytes_modeled", "status"],
+               [[r["tile_x1"], "" if r["seconds"] is None else r["seconds"],
+                 "" if r["bytes_modeled"] is None else r["bytes_modeled"], r["status"]] for r in rows])
+    return {"status": "ok", "best_tile_x1": best[1], "rows": rows, "artifacts": {"autotune_csv": str(csv_path)}}

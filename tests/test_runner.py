@@ -122,3 +122,23 @@ def test_execute_bench_profiles_and_solution_rows(tmp_path):
     f, b = hb.perf.model_counts("monolithic", 3, grid, cfg.step_config())
     assert out["runs"][1]["flops"] == f * 2 * 3 and out["runs"][1]["bytes"] == b * 2 * 3
     assert (tmp_path / "perf.json").exists() and (tmp_path / "perf.csv").exists()
+
+
+def test_execute_autotune_validates_candidates(tmp_path):
+    cfg = runner.RunConfig(order_n=1, cells=(8, 8, 8), steps=1, out_dir=str(tmp_path))
+    with pytest.raises(runner.ConfigError, match="candidates"):
+        runner.execute_autotune(cfg, [2])
+
+
+@pytest.mark.gpu
+def test_execute_autotune_table_and_selection(tmp_path):
+    """Reference runner.py:272-327 semantics: skipped rows for tiles wider than M1, one winner
+    (argmin of the median time, ties to the smaller tile), autotune.csv written."""
+    cfg = runner.RunConfig(order_n=3, cells=(12, 10, 8), steps=1, out_dir=str(tmp_path), variant="separable")
+    out = runner.execute_autotune(cfg, [2, 4, 64], repetitions=3)
+    status = {r["tile_x1"]: r["status"] for r in out["rows"]}
+    assert status[64].startswith("skipped") and list(status.values()).count("winner") == 1
+    assert status[out["best_tile_x1"]] == "winner" and out["best_tile_x1"] in (2, 4)
+    assert (tmp_path / "autotune.csv").read_text().splitlines()[0] == "tile_x1,seconds,bytes_modeled,status"
+    with pytest.raises(runner.ConfigError, match="no candidate"):
+        runner.execute_autotune(cfg, [64, 128])
