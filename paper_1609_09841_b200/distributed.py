@@ -157,10 +157,8 @@ class SlabSolver:
             # in-kernel p2p halo where it is available (N = 3, 5), verified against the NCCL copy
             # on the first initialised field (init); any failure falls back to NCCL
             if order_n in (3, 5):
-                try:
-                    self._setup_p2p()
-                except Exception as exc:  # noqa: BLE001 -- any mapping failure means "use NCCL"
-                    self.halo, self.halo_note = "nccl", f"p2p setup failed: {exc}"
+                if not self._setup_p2p(tolerant=True):  # collective: all ranks agree
+                    self.halo = "nccl"
             else:
                 self.halo, self.halo_note = "nccl", "p2p halo kernels exist for N = 3, 5"
         elif halo == "p2p":
@@ -197,18 +195,28 @@ class SlabSolver:
         fields fill HBM at 512^3 per GPU): the plane that reads the ghost is compared exactly,
         the whole field through a 64-bit checksum of its bits.  Leaves the fields stepped."""
         ok = True
-        try:
-            flag = torch.full((1,), -1, dtype=torch.int64, device="cuda")
-            L = self.local
-            for si, di, off, edge in ((0, 1, 0, L), (1, 0, -1, 1)):  # edge: buffer index of the ghost-reading plane
-                self._half_p2p(si, di, off, flag, False)
-                via_p2p = (self.bufs[di][1:-1].view(torch.int64).sum(), self.bufs[di][edge].clone())
-                self.half_step(self.bufs[si], self.bufs[di], off, flag)
-                ok = ok and bool(via_p2p[0] == self.bufs[di][1:-1].view(torch.int64).sum()) \
-                    and bool(torch.equal(via_p2p[1], self.bufs[di][edge]))
-                del via_p2p
-        except Exception as exc:  # noqa: BLE001
-            ok, self.halo_note = False, f"p2p verification raised: {exc}"
+
+        def attempt(fn):
+            # a local failure must not skip the collectives inside the later steps (the halo
+            # barrier / exchange): record it and carry on, the vote below decides for everyone
+            nonlocal ok
+            try:
+                return fn()
+            except Exception as exc:  # noqa: BLE001
+                ok = False
+                self.halo_note = self.halo_note or f"p2p verification raised: {exc}"
+                return None
+
+        flag = torch.full((1,), -1, dtype=torch.int64, device="cuda")
+        L = self.local
+        for si, di, off, edge in ((0, 1, 0, L), (1, 0, -1, 1)):  # edge: buffer index of the ghost-reading plane
+            attempt(lambda: self._half_p2p(si, di, off, flag, False))
+            via_p2p = attempt(lambda: (self.bufs[di][1:-1].view(torch.int64).sum(), self.bufs[di][edge].clone()))
+            attempt(lambda: self.half_step(self.bufs[si], self.bufs[di], off, flag))
+            same = attempt(lambda: bool(via_p2p[0] == self.bufs[di][1:-1].view(torch.int64).sum())
+                           and bool(torch.equal(via_p2p[1], self.bufs[di][edge])))
+            ok = ok and bool(same)
+            del via_p2p
         votes = torch.tensor([0.0 if ok else 1.0], device="cuda" if self.world == 1 or
                              dist.get_backend(self.group) == "nccl" else "cpu")
         if self.world > 1:
@@ -239,18 +247,37 @@ class SlabSolver:
             events.append((e0, e1))
 
     # ---- p2p halo: the kernel reads the neighbour's boundary plane in place (CUDA IPC / NVLink) ----
-    def _setup_p2p(self):
+    def _all_ranks_ok(self, ok: bool) -> bool:
+        """Collective AND of a per-rank verdict (every rank must call it)."""
+        if self.world == 1:
+            return ok
+        flag = torch.tensor([1 if ok else 0], dtype=torch.int64,
+                            device="cuda" if dist.get_backend(self.group) == "nccl" else "cpu")
+        dist.all_reduce(flag, op=dist.ReduceOp.MIN, group=self.group)
+        return bool(flag.item())
+
+    def _setup_p2p(self, tolerant: bool = False) -> bool:
         """Map the neighbours' field buffers (CUDA IPC handles exchanged through the process
-        group); with one rank the 'neighbours' are the rank itself (periodic wrap)."""
-        if self.order_n not in (3, 5):
-            raise NotImplementedError("the in-kernel p2p halo is implemented for N = 3 and 5")
+        group); with one rank the 'neighbours' are the rank itself (periodic wrap).
+
+        Collective and failure-consistent: every rank takes part in the handle exchange and in
+        the final verdict even if its own export or mapping failed, so either all ranks use the
+        p2p halo or none does (no rank is left waiting in a collective).  tolerant: report a
+        failure by returning False (the caller falls back to NCCL) instead of raising."""
         lib = _native.lib()
-        mine = []
-        for b in self.bufs:
-            h = (ctypes.c_ubyte * 64)()
-            off = ctypes.c_int64()
-            _native.check(lib.h3_ipc_export(ctypes.c_void_p(b.data_ptr()), h, ctypes.byref(off)), "h3_ipc_export")
-            mine.append((bytes(h), int(off.value), self.local))
+        mine, err = None, None
+        try:
+            if self.order_n not in (3, 5):
+                raise NotImplementedError("the in-kernel p2p halo is implemented for N = 3 and 5")
+            mine = []
+            for b in self.bufs:
+                h = (ctypes.c_ubyte * 64)()
+                off = ctypes.c_int64()
+                _native.check(lib.h3_ipc_export(ctypes.c_void_p(b.data_ptr()), h, ctypes.byref(off)),
+                              "h3_ipc_export")
+                mine.append((bytes(h), int(off.value), self.local))
+        except Exception as exc:  # noqa: BLE001 -- reported collectively below
+            err = exc
         everyone = [None] * self.world
         if self.world > 1:
             dist.all_gather_object(everyone, mine, group=self.group)
@@ -259,21 +286,36 @@ class SlabSolver:
         self._opened = []
         bases = {}  # IPC handle -> mapped allocation base
         self._peer = {}  # rank -> ([buf0 ptr, buf1 ptr], local planes); ptr = the ghosted buffer base
-        for r in {(self.rank - 1) % self.world, (self.rank + 1) % self.world}:
-            if r == self.rank:
-                self._peer[r] = ([b.data_ptr() for b in self.bufs], self.local)
-                continue
-            ptrs = []
-            for handle, offset, _ in everyone[r]:
-                if handle not in bases:  # both fields may live in one allocation: map it once
-                    base = ctypes.c_void_p()
-                    hb = (ctypes.c_ubyte * 64).from_buffer_copy(handle)
-                    _native.check(lib.h3_ipc_open(hb, ctypes.byref(base)), "h3_ipc_open")
-                    self._opened.append(base.value)
-                    bases[handle] = base.value
-                ptrs.append(bases[handle] + offset)
-            self._peer[r] = (ptrs, everyone[r][0][2])
+        if err is None:
+            try:
+                for r in {(self.rank - 1) % self.world, (self.rank + 1) % self.world}:
+                    if r == self.rank:
+                        self._peer[r] = ([b.data_ptr() for b in self.bufs], self.local)
+                        continue
+                    if everyone[r] is None:
+                        raise RuntimeError(f"rank {r} could not export its field buffers")
+                    ptrs = []
+                    for handle, offset, _ in everyone[r]:
+                        if handle not in bases:  # both fields may live in one allocation: map it once
+                            base = ctypes.c_void_p()
+                            hb = (ctypes.c_ubyte * 64).from_buffer_copy(handle)
+                            _native.check(lib.h3_ipc_open(hb, ctypes.byref(base)), "h3_ipc_open")
+                            self._opened.append(base.value)
+                            bases[handle] = base.value
+                        ptrs.append(bases[handle] + offset)
+                    self._peer[r] = (ptrs, everyone[r][0][2])
+            except Exception as exc:  # noqa: BLE001
+                err = exc
+        if not self._all_ranks_ok(err is None):
+            self.close()
+            self._peer = {}
+            reason = f"p2p setup failed: {err}" if err is not None else "p2p setup failed on another rank"
+            if tolerant:
+                self.halo_note = reason
+                return False
+            raise RuntimeError(reason) from err
         self._sync = torch.zeros(1, device="cuda")
+        return True
 
     def _barrier(self):
         """Stream-ordered rendezvous: every rank's previous half step is complete (its planes are

@@ -144,3 +144,48 @@ def test_slab_solver_instability_is_collective(halo, tmp_path):
     mp.start_processes(_bad_worker, args=(2, _free_port(), (8, 7, 8), (5, 2, 3, 0, 0, 0), halo, str(out)),
                        nprocs=2, join=True, start_method="spawn")
     assert out.read_text() == "ok"
+
+
+def _fail_worker(rank, world, port, result_path):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import paper_1609_09841_b200 as hb
+        from paper_1609_09841_b200 import _native
+        from paper_1609_09841_b200.distributed import SlabSolver
+        torch.cuda.set_device(0)
+        if rank == 1:  # this rank cannot export its buffers (e.g. no IPC support)
+            _native.lib().h3_ipc_export = lambda *args: -1
+        cells = (16, 14, 12)
+        cfg = hb.StepConfig(variant="separable")
+        solver = SlabSolver(cells, 3, cfg, halo="auto")
+        solver.init(hb.plane_wave())
+        for _ in range(2):
+            solver.step()
+        solver.check()
+        halos = [None] * world
+        dist.all_gather_object(halos, (solver.halo, solver.halo_note))
+        states = [None] * world
+        dist.all_gather_object(states, solver.state.cpu())
+        if rank == 0:
+            grid = hb.GridSpec(cells)
+            state = hb.init_field(hb.plane_wave(), grid, 3)
+            scratch = hb.DofField.zeros(grid.with_parity("dual"), 3)
+            for _ in range(2):
+                hb.full_step(state, scratch, cfg, hb.OperatorSet.for_grid(grid, 3), dt=solver.dt)
+            ok = all(h == "nccl" and "p2p setup failed" in note for h, note in halos) \
+                and torch.equal(torch.cat(states), state.tensor.cpu())
+            with open(result_path, "w") as fh:
+                fh.write("ok" if ok else f"mismatch {halos}")
+        dist.barrier()
+        solver.close()
+    finally:
+        dist.destroy_process_group()
+
+
+def test_slab_solver_p2p_setup_failure_on_one_rank_falls_back_everywhere(tmp_path):
+    """halo="auto": when one rank cannot set up the IPC mapping, every rank agrees on the NCCL
+    halo (no rank waits in a collective the others skipped) and the result is unchanged."""
+    out = tmp_path / "result.txt"
+    mp.start_processes(_fail_worker, args=(2, _free_port(), str(out)), nprocs=2, join=True, start_method="spawn")
+    assert out.read_text() == "ok"
