@@ -501,3 +501,16 @@ def test_run_steps_graph_reports_instability_step():
     with pytest.raises(hb.InstabilityError) as err:
         hb.run_steps(st, sc, cfg, ops, 20, first_step=5, graph=True)
     assert err.value.step == 5
+
+
+def test_pure_c_host_through_the_c_abi():
+    """examples/c_host_step.c drives the step through include/h3b200.h alone (no Python, no
+    torch): device init, 4 fused separable full steps, device error norms -- the node error
+    matches the reference's golden l_inf for N=3, 16^3, 4 steps."""
+    import subprocess
+    from pathlib import Path
+    exe = Path(__file__).resolve().parent.parent / "examples" / "c_host_step"
+    assert exe.exists(), "built by __graft_entry__.build()"
+    out = subprocess.run([str(exe)], capture_output=True, text=True, timeout=120)
+    assert out.returncode == 0, out.stdout + out.stderr
+    assert "l_inf=2.3857" in out.stdout
