@@ -389,9 +389,13 @@ def main():
         print(f"[bench] e2e {result['e2e']}", file=sys.stderr, flush=True)
     # ---- CPU baseline (rank 0, N = 1) ----------------------------------------------------------
     if world == 1 and not args.no_cpu:
-        rate, info = cpu_oracle_rate(order_n, cpu_sample_cells(order_n), args.cpu_seconds)
-        result["cpu_baseline"] = {"value": rate, "unit": UNIT, "cores": info["cores"], "kind": "port", "cpu": cpu_model(),
-                                  "sample": info["sample"]}
+        try:
+            rate, info = cpu_oracle_rate(order_n, cpu_sample_cells(order_n), args.cpu_seconds)
+            result["cpu_baseline"] = {"value": rate, "unit": UNIT, "cores": info["cores"], "kind": "port",
+                                      "cpu": cpu_model(), "sample": info["sample"]}
+        except (OSError, RuntimeError, subprocess.CalledProcessError) as exc:
+            result["cpu_baseline"] = {"value": None, "unit": UNIT, "cores": 0, "kind": "port",
+                                      "error": f"{type(exc).__name__}: {exc}"[:300]}
     if world == 1 and not args.no_extras:
         del state, scratch
         torch.cuda.empty_cache()
