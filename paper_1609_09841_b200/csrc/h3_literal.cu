@@ -141,15 +141,18 @@ literal_kernel(const T* __restrict__ in, T* __restrict__ out, Dims d, int off,
         bufA[(z * S + y) * S + x] = ru[x];
     }
     __syncthreads();
+    // this thread's y / z factors are stage-invariant: load them once (a per-thread index into the
+    // parameter bank would otherwise be re-read, serialised across the warp, every stage)
+    const T f2y = p.f2[y], f3z = p.f3[z], zero = p.f1[S - 1];
     for (int k = p.q; k >= 1; --k) {
         const T c = p.cf[k - 1];
         T nw[S];
 #pragma unroll
         for (int x = 0; x < S; ++x) {
-            T acc = p.f1[S - 1];  // the reference's typed zero
+            T acc = zero;  // the reference's typed zero
             if (x < S - 1) acc = RN<T>::add(acc, RN<T>::mul(p.f1[x], w[x + 1]));
-            if (y < S - 1) acc = RN<T>::add(acc, RN<T>::mul(p.f2[y], bufA[(z * S + y + 1) * S + x]));
-            if (z < S - 1) acc = RN<T>::add(acc, RN<T>::mul(p.f3[z], bufA[((z + 1) * S + y) * S + x]));
+            if (y < S - 1) acc = RN<T>::add(acc, RN<T>::mul(f2y, bufA[(z * S + y + 1) * S + x]));
+            if (z < S - 1) acc = RN<T>::add(acc, RN<T>::mul(f3z, bufA[((z + 1) * S + y) * S + x]));
             nw[x] = RN<T>::add(ru[x], RN<T>::mul(c, acc));
         }
         __syncthreads();
