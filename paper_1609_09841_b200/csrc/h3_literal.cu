@@ -132,6 +132,16 @@ literal_kernel(const T* __restrict__ in, T* __restrict__ out, Dims d, int off,
     }
 
     // ---- evolve (gridkernels.py:86-110): q-stage Horner, two-phase --------------
+    // Stage k reads the neighbours' stage-(k-1) values from `cur` and writes its own to `nxt`
+    // (the two buffers alternate), so one barrier per stage orders both the reads after the
+    // writes and the next overwrite after the reads.  When a cell's threads are whole warps
+    // (N = 3: 64 threads) the barrier is the cell's own named barrier, not the CTA's.
+    auto cell_sync = [&]() {
+        if constexpr (CPB > 1 && S2 % 32 == 0)
+            asm volatile("bar.sync %0, %1;" ::"r"(1 + local), "n"(S2) : "memory");
+        else
+            __syncthreads();
+    };
     const int z = t / S, y = t % S;
     T ru[S], w[S];
 #pragma unroll
@@ -141,6 +151,8 @@ literal_kernel(const T* __restrict__ in, T* __restrict__ out, Dims d, int off,
         bufA[(z * S + y) * S + x] = ru[x];
     }
     __syncthreads();
+    T* cur = bufA;
+    T* nxt = bufB;
     // this thread's y / z factors are stage-invariant: load them once (a per-thread index into the
     // parameter bank would otherwise be re-read, serialised across the warp, every stage)
     const T f2y = p.f2[y], f3z = p.f3[z], zero = p.f1[S - 1];
@@ -151,17 +163,19 @@ literal_kernel(const T* __restrict__ in, T* __restrict__ out, Dims d, int off,
         for (int x = 0; x < S; ++x) {
             T acc = zero;  // the reference's typed zero
             if (x < S - 1) acc = RN<T>::add(acc, RN<T>::mul(p.f1[x], w[x + 1]));
-            if (y < S - 1) acc = RN<T>::add(acc, RN<T>::mul(f2y, bufA[(z * S + y + 1) * S + x]));
-            if (z < S - 1) acc = RN<T>::add(acc, RN<T>::mul(f3z, bufA[((z + 1) * S + y) * S + x]));
+            if (y < S - 1) acc = RN<T>::add(acc, RN<T>::mul(f2y, cur[(z * S + y + 1) * S + x]));
+            if (z < S - 1) acc = RN<T>::add(acc, RN<T>::mul(f3z, cur[((z + 1) * S + y) * S + x]));
             nw[x] = RN<T>::add(ru[x], RN<T>::mul(c, acc));
         }
-        __syncthreads();
 #pragma unroll
         for (int x = 0; x < S; ++x) {
             w[x] = nw[x];
-            bufA[(z * S + y) * S + x] = nw[x];
+            nxt[(z * S + y) * S + x] = nw[x];
         }
-        __syncthreads();
+        cell_sync();
+        T* const tmp = cur;
+        cur = nxt;
+        nxt = tmp;
     }
     // ---- scatter (gridkernels.py:113-118) -----------------------------------------
     if (valid && z < n && y < n) {
