@@ -42,6 +42,10 @@ literal_kernel(const T* __restrict__ in, T* __restrict__ out, Dims d, int off,
                const __grid_constant__ LitOps<T, N> p, unsigned long long* first_bad,
                const unsigned long long* guard) {
     constexpr int n = N + 1, S = 2 * n, S2 = S * S, S3 = S2 * S, n3 = n * n * n;
+    // shared tensors [a][b][c] with the innermost stride padded to SP = S + 1: the lanes of every
+    // sweep and of the Horner stages then hit distinct banks (an unpadded 8-double row stride put
+    // 8 lanes of a half-warp on the same bank pair at N = 3)
+    constexpr int SP = S + 1, SB = S2 * SP;
     using A = Arith<T, FAST>;
     if (guarded_out(guard, first_bad)) return;
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -49,8 +53,8 @@ literal_kernel(const T* __restrict__ in, T* __restrict__ out, Dims d, int off,
 
     const int local = threadIdx.x / S2;
     const int t = threadIdx.x % S2;
-    T* bufA = sm + (size_t)local * 2 * S3;
-    T* bufB = bufA + S3;
+    T* bufA = sm + (size_t)local * 2 * SB;
+    T* bufB = bufA + SB;
 
     const int64_t nxy = d.M1 * d.M2;
     const int64_t total = (d.z_end - d.z_begin) * nxy;
@@ -69,7 +73,7 @@ literal_kernel(const T* __restrict__ in, T* __restrict__ out, Dims d, int off,
                 const int64_t g3 = zplane(c3 + off + a3, d.M3, d.periodic_z);
                 const int64_t g2 = wrap(c2 + off + a2, d.M2);
                 const int64_t g1 = wrap(c1 + off + a1, d.M1);
-                bufA[e] = in[((g3 * d.M2 + g2) * d.M1 + g1) * n3 + (j3 * n + j2) * n + j1];
+                bufA[(zz * S + yy) * SP + xx] = in[((g3 * d.M2 + g2) * d.M1 + g1) * n3 + (j3 * n + j2) * n + j1];
             }
         }
         __syncthreads();
@@ -78,13 +82,13 @@ literal_kernel(const T* __restrict__ in, T* __restrict__ out, Dims d, int off,
             const int o = t / S, m = t % S;  // (z, y)
             T u[S];
 #pragma unroll
-            for (int k = 0; k < S; ++k) u[k] = bufA[(o * S + m) * S + k];
+            for (int k = 0; k < S; ++k) u[k] = bufA[(o * S + m) * SP + k];
 #pragma unroll
             for (int i = 0; i < S; ++i) {
                 T c = A::mul(p.H[i * S], u[0]);
 #pragma unroll
                 for (int k = 1; k < S; ++k) c = A::mac(c, p.H[i * S + k], u[k]);
-                bufB[(o * S + m) * S + i] = c;
+                bufB[(o * S + m) * SP + i] = c;
             }
         }
         __syncthreads();
@@ -92,13 +96,13 @@ literal_kernel(const T* __restrict__ in, T* __restrict__ out, Dims d, int off,
             const int o = t / S, x = t % S;  // (z, x)
             T u[S];
 #pragma unroll
-            for (int k = 0; k < S; ++k) u[k] = bufB[(o * S + k) * S + x];
+            for (int k = 0; k < S; ++k) u[k] = bufB[(o * S + k) * SP + x];
 #pragma unroll
             for (int i = 0; i < S; ++i) {
                 T c = A::mul(p.H[i * S], u[0]);
 #pragma unroll
                 for (int k = 1; k < S; ++k) c = A::mac(c, p.H[i * S + k], u[k]);
-                bufA[(o * S + i) * S + x] = c;
+                bufA[(o * S + i) * SP + x] = c;
             }
         }
         __syncthreads();
@@ -106,27 +110,27 @@ literal_kernel(const T* __restrict__ in, T* __restrict__ out, Dims d, int off,
             const int y = t / S, x = t % S;  // (y, x)
             T u[S];
 #pragma unroll
-            for (int k = 0; k < S; ++k) u[k] = bufA[(k * S + y) * S + x];
+            for (int k = 0; k < S; ++k) u[k] = bufA[(k * S + y) * SP + x];
 #pragma unroll
             for (int i = 0; i < S; ++i) {
                 T c = A::mul(p.H[i * S], u[0]);
 #pragma unroll
                 for (int k = 1; k < S; ++k) c = A::mac(c, p.H[i * S + k], u[k]);
-                bufB[(i * S + y) * S + x] = c;
+                bufB[(i * S + y) * SP + x] = c;
             }
         }
         __syncthreads();
         if (MODE == 1) {
             if (valid) {
                 T* dstc = out + (size_t)cell * S3;  // chunk-relative cell index
-                for (int e = t; e < S3; e += S2) dstc[e] = bufB[e];
+                for (int e = t; e < S3; e += S2) dstc[e] = bufB[(e / S) * SP + e % S];
             }
             return;
         }
     } else {
         if (valid) {
             const T* srcc = in + (size_t)cell * S3;
-            for (int e = t; e < S3; e += S2) bufB[e] = srcc[e];
+            for (int e = t; e < S3; e += S2) bufB[(e / S) * SP + e % S] = srcc[e];
         }
         __syncthreads();
     }
@@ -146,9 +150,9 @@ literal_kernel(const T* __restrict__ in, T* __restrict__ out, Dims d, int off,
     T ru[S], w[S];
 #pragma unroll
     for (int x = 0; x < S; ++x) {
-        ru[x] = bufB[(z * S + y) * S + x];
+        ru[x] = bufB[(z * S + y) * SP + x];
         w[x] = ru[x];
-        bufA[(z * S + y) * S + x] = ru[x];
+        bufA[(z * S + y) * SP + x] = ru[x];
     }
     __syncthreads();
     T* cur = bufA;
@@ -163,14 +167,14 @@ literal_kernel(const T* __restrict__ in, T* __restrict__ out, Dims d, int off,
         for (int x = 0; x < S; ++x) {
             T acc = zero;  // the reference's typed zero
             if (x < S - 1) acc = RN<T>::add(acc, RN<T>::mul(p.f1[x], w[x + 1]));
-            if (y < S - 1) acc = RN<T>::add(acc, RN<T>::mul(f2y, cur[(z * S + y + 1) * S + x]));
-            if (z < S - 1) acc = RN<T>::add(acc, RN<T>::mul(f3z, cur[((z + 1) * S + y) * S + x]));
+            if (y < S - 1) acc = RN<T>::add(acc, RN<T>::mul(f2y, cur[(z * S + y + 1) * SP + x]));
+            if (z < S - 1) acc = RN<T>::add(acc, RN<T>::mul(f3z, cur[((z + 1) * S + y) * SP + x]));
             nw[x] = RN<T>::add(ru[x], RN<T>::mul(c, acc));
         }
 #pragma unroll
         for (int x = 0; x < S; ++x) {
             w[x] = nw[x];
-            nxt[(z * S + y) * S + x] = nw[x];
+            nxt[(z * S + y) * SP + x] = nw[x];
         }
         cell_sync();
         T* const tmp = cur;
@@ -195,10 +199,10 @@ template <typename T, int N, int MODE, bool FAST>
 static int launch_one(const T* in, T* out, const Dims& d, const LitOps<T, N>& ops, int off,
                       cudaStream_t st, unsigned long long* first_bad,
                       const unsigned long long* guard) {
-    constexpr int S = 2 * N + 2, S2 = S * S, S3 = S2 * S, CPB = lit_cpb<N>();
+    constexpr int S = 2 * N + 2, S2 = S * S, S3 = S2 * S, CPB = lit_cpb<N>(), SB = S2 * (S + 1);
     const int64_t total = (d.z_end - d.z_begin) * d.M1 * d.M2;
     if (total <= 0) return 0;
-    const size_t smem = (size_t)CPB * 2 * S3 * sizeof(T);
+    const size_t smem = (size_t)CPB * 2 * SB * sizeof(T);
     auto kern = literal_kernel<T, N, CPB, MODE, FAST>;
     // per-device attribute; cheap and idempotent, so set on every launch
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
