@@ -199,7 +199,7 @@ template <typename T, int N, int MODE, bool FAST>
 static int launch_one(const T* in, T* out, const Dims& d, const LitOps<T, N>& ops, int off,
                       cudaStream_t st, unsigned long long* first_bad,
                       const unsigned long long* guard) {
-    constexpr int S = 2 * N + 2, S2 = S * S, S3 = S2 * S, CPB = lit_cpb<N>(), SB = S2 * (S + 1);
+    constexpr int S = 2 * N + 2, S2 = S * S, CPB = lit_cpb<N>(), SB = S2 * (S + 1);
     const int64_t total = (d.z_end - d.z_begin) * d.M1 * d.M2;
     if (total <= 0) return 0;
     const size_t smem = (size_t)CPB * 2 * SB * sizeof(T);
