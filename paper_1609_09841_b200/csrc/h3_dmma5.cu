@@ -314,7 +314,9 @@ struct Cfg {
     static constexpr int WARPS = 16, THREADS = 32 * WARPS, STAGES = STAGES_;
     static constexpr int UNS = n3;
     static constexpr int WI = n2 + 1, WCS = S * WI;  // W: [node row][cell][i1][j3 j2]
-    static constexpr int VJ = S2 + 1, VCS = n * VJ;  // V: [cell][j3][i2 i1]
+    // V: [cell][j3][i2 i1]; j3 stride = 4 (mod 16 doubles) so the x3 A-fragment loads (8 lines x 4
+    // k of one cell) fall on 16 distinct bank pairs per half-warp (S2 + 1 gave 8-way conflicts)
+    static constexpr int VJ = S2 + 4, VCS = n * VJ;
     static constexpr int L1 = NY * TX * n2, L2 = TY * TX * n * S, L3 = TY * TX * S2;
     static constexpr int G1 = (L1 + 7) / 8, G2 = (L2 + 7) / 8, G3 = (L3 + 7) / 8;
     static constexpr size_t U_D = (size_t)NNODE * UNS;
