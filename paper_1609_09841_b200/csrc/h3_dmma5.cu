@@ -100,7 +100,13 @@ sep_fused_dmma_cp_kernel(const double* __restrict__ src, double* __restrict__ ds
 #pragma unroll
     for (int ax = 0; ax < 3; ++ax)
 #pragma unroll
-        for (int ks = 0; ks < KS; ++ks) bop[ax][ks] = g < n ? p.A[ax][g < n ? g : 0][4 * ks + q] : 0.0;
+        for (int ks = 0; ks < KS; ++ks) {
+            // x1 orders its K inputs as (vertex q >> 1, component 2 ks + (q & 1)) instead of
+            // k = 4 ks + q: with the 6-double line rows of a node block this puts the 16 lanes of a
+            // half-warp on 16 distinct bank pairs (found by search; the natural order is 2-way)
+            const int kc = (ax == 0 && C::N == 5) ? (q >> 1) * n + 2 * ks + (q & 1) : 4 * ks + q;
+            bop[ax][ks] = g < n ? p.A[ax][g < n ? g : 0][kc] : 0.0;
+        }
 
     // loader: lane 0 of warp ly < NY copies tile row ly of every plane
     int rowoff = 0, gx0 = 0;
@@ -151,7 +157,8 @@ sep_fused_dmma_cp_kernel(const double* __restrict__ src, double* __restrict__ ds
     for (int ks = 0; ks < KS; ++ks) {
         const int k = 4 * ks + q, a = k / n, j = k % n;
         ka[ks] = a;
-        k1[ks] = a * UNS + j;      // x1: node cx + a along the row
+        k1[ks] = C::N == 5 ? (q >> 1) * UNS + 2 * ks + (q & 1)  // x1: permuted K (see bop)
+                           : a * UNS + j;                        // x1: node cx + a along the row
         k2[ks] = a * TX * WCS + j; // x2: cell row cy + a
         k3[ks] = j * VJ;           // x3: V slot of plane p - 1 + a
     }
