@@ -38,6 +38,18 @@ using tma::mbar_fence_init;
 using tma::mbar_init;
 using tma::mbar_wait;
 
+// K order of the N = 5 fused passes: the input c = a n + j (vertex a, component j) that lane q
+// reads at k-step ks, per pass (x1, x2, x3).  Found by tools/cp5_korder_search.py: a half-warp's
+// 4 lines x 4 k-lanes then fall on distinct bank pairs (x1) or fewer wavefronts (x2),
+// where the natural order k = 4 ks + q is 2-way on every load.  Packed 4 bits per lane q.
+__device__ __forceinline__ int korder5(int ax, int ks, int q) {
+    constexpr unsigned T[3][3] = {{0x7610u, 0x9832u, 0xba54u},   // x1: (q >> 1, 2 ks + (q & 1))
+                                  {0xa640u, 0xb751u, 0x9832u},   // x2
+                                  {0x3210u, 0x7654u, 0xba98u}};  // x3: natural (the searched
+                                  // conflict-free 0x6210 0xa843 0xb975 measured 4 % slower)
+    return (int)((T[ax][ks] >> (4 * q)) & 15u);
+}
+
 // group `warp + WARPS * it` of a pass with G groups of 8 lines exists (warp-uniform; constant
 // true when the groups divide evenly, so the unrolled loops keep no test)
 template <int G, int WARPS>
@@ -104,7 +116,7 @@ sep_fused_dmma_cp_kernel(const double* __restrict__ src, double* __restrict__ ds
             // x1 orders its K inputs as (vertex q >> 1, component 2 ks + (q & 1)) instead of
             // k = 4 ks + q: with the 6-double line rows of a node block this puts the 16 lanes of a
             // half-warp on 16 distinct bank pairs (found by search; the natural order is 2-way)
-            const int kc = (ax == 0 && C::N == 5) ? (q >> 1) * n + 2 * ks + (q & 1) : 4 * ks + q;
+            const int kc = C::N == 5 ? korder5(ax, ks, q) : 4 * ks + q;
             bop[ax][ks] = g < n ? p.A[ax][g < n ? g : 0][kc] : 0.0;
         }
 
@@ -155,12 +167,14 @@ sep_fused_dmma_cp_kernel(const double* __restrict__ src, double* __restrict__ ds
     int k1[KS], k2[KS], k3[KS], ka[KS];
 #pragma unroll
     for (int ks = 0; ks < KS; ++ks) {
-        const int k = 4 * ks + q, a = k / n, j = k % n;
-        ka[ks] = a;
-        k1[ks] = C::N == 5 ? (q >> 1) * UNS + 2 * ks + (q & 1)  // x1: permuted K (see bop)
-                           : a * UNS + j;                        // x1: node cx + a along the row
-        k2[ks] = a * TX * WCS + j; // x2: cell row cy + a
-        k3[ks] = j * VJ;           // x3: V slot of plane p - 1 + a
+        // per pass, the (vertex a, component j) this lane's k-slot reads (korder5: N = 5)
+        const int c1 = C::N == 5 ? korder5(0, ks, q) : 4 * ks + q;
+        const int c2 = C::N == 5 ? korder5(1, ks, q) : 4 * ks + q;
+        const int c3 = C::N == 5 ? korder5(2, ks, q) : 4 * ks + q;
+        k1[ks] = (c1 / n) * UNS + c1 % n;       // x1: node cx + a along the row
+        k2[ks] = (c2 / n) * TX * WCS + c2 % n;  // x2: cell row cy + a
+        ka[ks] = c3 / n;                        // x3: plane p - 1 + a ...
+        k3[ks] = (c3 % n) * VJ;                 //     ... its j3 slot
     }
     const bool qout = 2 * q < n;  // this lane's output columns 2q, 2q + 1 are real outputs
     int r1[I1], w1[I1], r2[I2], w2[I2], r3[I3], o3[I3];
