@@ -70,3 +70,52 @@ for name, la, ka, L in (("x2", x2_line, x2_k, TY * TX * n2), ("x3", x3_line, x3_
     base = cost(natural, la, ka, L)
     best = min(partitions(), key=lambda p: cost(p, la, ka, L))
     print(name, "natural", base, "best", cost(best, la, ka, L), best)
+
+
+# ---- the m=5 reconstruction (rcp::Cfg<5, 4, 2, 2>): one K order shared by its three passes
+# (all of them contract with the same H, so one set of B fragments) --------------------------
+RTX, RTY, RNX, RNY = 4, 2, 5, 3
+S = 2 * n
+UNS = n ** 3
+RWI, RWCS = n2 + 1, S * (n2 + 1)   # W [row][cell][i1][j3 j2]
+RVJ, RVCS = S * S + 4, n * (S * S + 4)  # V [cell][j3][i2 i1]
+
+
+def r1_line(l):
+    rc, jj = divmod(l, n2)
+    ly, cx = divmod(rc, RTX)
+    return (ly * RNX + cx) * UNS + jj * n
+
+
+def r1_k(a, j):
+    return a * UNS + j
+
+
+def r2_line(l):
+    cell, r = divmod(l, n * S)
+    j3, i1 = divmod(r, S)
+    return cell * RWCS + i1 * RWI + j3 * n
+
+
+def r2_k(a, j):
+    return a * RTX * RWCS + j
+
+
+def r3_line(l):
+    cell, r = divmod(l, S * S)
+    return cell * RVCS + r
+
+
+def r3_k(a, j):
+    return j * RVJ
+
+
+def recon_cost(p):
+    return (cost(p, r1_line, r1_k, RNY * RTX * n2) + cost(p, r2_line, r2_k, RTY * RTX * n * S)
+            + cost(p, r3_line, r3_k, RTY * RTX * S * S))
+
+
+if __name__ == "__main__":
+    base = recon_cost(natural)
+    best = min(partitions(), key=recon_cost)
+    print("recon natural", base, "best", recon_cost(best), best)
