@@ -5,7 +5,7 @@ cp $L /tmp/new.so
 {
 timeout 900 python -m pytest tests -q -x -m gpu -k "separable or fused or two_pass or recon or degenerate" 2>&1 | tail -1
 for r in 1 2; do
-  for mode in fused; do
+  for mode in two_pass; do
     cp paper_1609_09841_b200/libh3b200_old.so $L; echo -n "old "; timeout 300 python tools/time_fused.py 5 256 $mode 4
     cp /tmp/new.so $L; echo -n "new "; timeout 300 python tools/time_fused.py 5 256 $mode 4
   done
