@@ -53,7 +53,7 @@ extern "C" {
 /* negative status codes */
 #define H3_ERR_ARG -1     /* null pointer, bad size, bad offset or slab range   */
 #define H3_ERR_ORDER -2   /* order_n outside [0, h3_max_order()]                */
-#define H3_ERR_STAGES -3  /* q outside [1, h3_max_stages()], or separable with q < 3(2N+1) */
+#define H3_ERR_STAGES -3  /* q < 1, literal with q > h3_max_stages(), or separable with q < 3(2N+1) */
 #define H3_ERR_VARIANT -4 /* variant not available for this precision/kernel    */
 
 /* Replaces gridkernels.fused_pass(src, dst, h_mat, fac1, fac2, fac3, cfac, tiles, off)

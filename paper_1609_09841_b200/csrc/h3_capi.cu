@@ -66,7 +66,7 @@ static int fused_impl(const T* src, T* dst, int64_t M1, int64_t M2, int64_t M3, 
     if (rc) return rc;
     if (!src || !dst || !h_mat || !fac1 || !fac2 || !fac3 || !cfac) return H3_ERR_ARG;
     if (off != 0 && off != -1) return H3_ERR_ARG;
-    if (q < 1 || q > H3_MAX_STAGES) return H3_ERR_STAGES;
+    if (q < 1) return H3_ERR_STAGES;
     Dims d{M1, M2, M3, z_begin, z_end, periodic_z ? 1 : 0};
     cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
     bool separable;
@@ -89,6 +89,9 @@ static int fused_impl(const T* src, T* dst, int64_t M1, int64_t M2, int64_t M3, 
         return h3::sep_fused_launch((const double*)src, (double*)dst, d, order_n, A, off, st,
                                     d_first_bad, d_guard);
     }
+    // the literal kernels keep the q stage factors in a fixed-size parameter block; the
+    // separable path uses cfac[0] only, so the cap applies here alone
+    if (q > H3_MAX_STAGES) return H3_ERR_STAGES;
     return h3::literal_launch<T>(0, false, src, dst, d, order_n, h_mat, fac1, fac2, fac3, cfac, q,
                                  off, st, d_first_bad, d_guard);
 }
@@ -145,7 +148,7 @@ static int evolve_impl(const T* coeff, T* dst, int64_t M1, int64_t M2, int64_t M
     int rc = check_common(M1, M2, M3, order_n, z_begin, z_end);
     if (rc) return rc;
     if (!coeff || !dst || !fac1 || !fac2 || !fac3 || !cfac) return H3_ERR_ARG;
-    if (q < 1 || q > H3_MAX_STAGES) return H3_ERR_STAGES;
+    if (q < 1) return H3_ERR_STAGES;
     bool separable;
     switch (variant) {
         case H3_VARIANT_AUTO: separable = sizeof(T) == 8 && q >= exact_stages(order_n); break;
@@ -170,6 +173,7 @@ static int evolve_impl(const T* coeff, T* dst, int64_t M1, int64_t M2, int64_t M
         return h3::sep_evolve_launch((const double*)coeff, (double*)dst, d, order_n, Sh, st,
                                      d_first_bad, d_guard);
     }
+    if (q > H3_MAX_STAGES) return H3_ERR_STAGES;  // literal only (see fused_impl)
     return h3::literal_launch<T>(2, false, coeff, dst, d, order_n, nullptr, fac1, fac2, fac3, cfac,
                                  q, 0, st, d_first_bad, d_guard);
 }
@@ -186,7 +190,6 @@ static int fused_halo_impl(const double* src, double* dst, int64_t M1, int64_t M
     if (off != 0 && off != -1) return H3_ERR_ARG;
     if (off == 0 && z_end == M3 && !ghost_hi) return H3_ERR_ARG;   // cell M3-1 reads plane M3
     if (off == -1 && z_begin == 0 && !ghost_lo) return H3_ERR_ARG;  // cell 0 reads plane -1
-    if (q < 1 || q > H3_MAX_STAGES) return H3_ERR_STAGES;
     if (q < exact_stages(order_n)) return H3_ERR_STAGES;
     // the tile-march kernels with TMA plane loads take the ghost pointers (N = 3, 5)
     if ((variant != H3_VARIANT_AUTO && variant != H3_VARIANT_SEPARABLE) || (order_n != 3 && order_n != 5))

@@ -143,6 +143,7 @@ class SlabSolver:
         self.ops = OperatorSet.for_grid(self.grid, order_n)
         self.dt = select_dt(self.grid, cfg)
         self.flags = torch.full((2,), -1, dtype=torch.int64, device="cuda")
+        self._guard = torch.full((1,), -1, dtype=torch.int64, device="cuda")
         self.kernel_events = []
         q = cfg.stages(order_n)
         self._fac = _factor_arrays(self.ops, np.float64, self.dt / 2, q)
@@ -227,7 +228,7 @@ class SlabSolver:
             self.halo = "nccl"
             self.halo_note = self.halo_note or "p2p result differed from the NCCL halo"
 
-    def _launch(self, src, dst, off, zb, ze, flag, events):
+    def _launch(self, src, dst, off, zb, ze, flag, events, guard=None):
         m1, m2, _ = self.grid.cells_per_axis
         h_mat, f1, f2, f3, cf = self._fac
         plane = src[0].numel() * src.element_size()
@@ -239,7 +240,7 @@ class SlabSolver:
             ctypes.c_void_p(src.data_ptr() + plane), ctypes.c_void_p(dst.data_ptr() + plane),
             m1, m2, self.local, self.order_n, _ptr(h_mat), _ptr(f1), _ptr(f2), _ptr(f3), _ptr(cf),
             self._q, off, zb, ze, 0, _native.VARIANTS[self.cfg.variant], ctypes.c_void_p(stream.cuda_stream),
-            ctypes.c_void_p(flag.data_ptr()), None)
+            ctypes.c_void_p(flag.data_ptr()), None if guard is None else ctypes.c_void_p(guard.data_ptr()))
         _native.check(rc, "h3_fused_pass (slab)")
         if e0 is not None:
             e1 = torch.cuda.Event(enable_timing=True)
@@ -328,12 +329,35 @@ class SlabSolver:
             torch.cuda.synchronize()
             dist.barrier(group=self.group)
 
-    def _half_p2p(self, si, di, off, flag, timed):
+    def _any_bad(self, flag: torch.Tensor) -> torch.Tensor:
+        """Device guard for the second half step: != -1 when the first half step failed on ANY
+        rank (all-reduce MAX of the signed flags; -1 = no bad node), so every rank skips it and
+        leaves its state untouched, as the reference does after raising (pipeline.py:274).
+        Stream-ordered under NCCL; it also orders the ranks' first half steps before the second
+        (the p2p halo's rendezvous)."""
+        if self.world == 1:
+            return flag
+        if dist.get_backend(self.group) == "nccl":
+            self._guard.copy_(flag)
+            dist.all_reduce(self._guard, op=dist.ReduceOp.MAX, group=self.group)
+            return self._guard
+        torch.cuda.synchronize()  # gloo (tests: several ranks sharing one GPU)
+        host = flag.cpu()
+        dist.all_reduce(host, op=dist.ReduceOp.MAX, group=self.group)
+        self._guard.copy_(host)
+        return self._guard
+
+    def _half_p2p(self, si, di, off, flag, timed, guard=None, collective_guard=False):
+        """One p2p-halo half step.  collective_guard: `guard` is this rank's flag of the previous
+        half step; the rendezvous becomes its all-reduce (_any_bad), one collective either way."""
         m1, m2, _ = self.grid.cells_per_axis
         h_mat, f1, f2, f3, cf = self._fac
         src, dst = self.bufs[si], self.bufs[di]
         plane = src[0].numel() * src.element_size()
-        self._barrier()
+        if collective_guard:
+            guard = self._any_bad(guard)
+        else:
+            self._barrier()
         glo = ghi = None
         if off == 0:  # cell L-1 reads node plane L = rank+1's first local plane
             ptrs, _ = self._peer[(self.rank + 1) % self.world]
@@ -349,7 +373,7 @@ class SlabSolver:
             ctypes.c_void_p(src.data_ptr() + plane), ctypes.c_void_p(dst.data_ptr() + plane), m1, m2, self.local,
             self.order_n, _ptr(h_mat), _ptr(f1), _ptr(f2), _ptr(f3), _ptr(cf), self._q, off, 0, self.local,
             glo, ghi, _native.VARIANTS[self.cfg.variant], ctypes.c_void_p(stream.cuda_stream),
-            ctypes.c_void_p(flag.data_ptr()), None)
+            ctypes.c_void_p(flag.data_ptr()), None if guard is None else ctypes.c_void_p(guard.data_ptr()))
         _native.check(rc, "h3_fused_pass_halo")
         if e0 is not None:
             e1 = torch.cuda.Event(enable_timing=True)
@@ -362,32 +386,40 @@ class SlabSolver:
             _native.lib().h3_ipc_close(ctypes.c_void_p(base))
         self._opened = []
 
-    def half_step(self, src, dst, off, flag, timed=False):
+    def half_step(self, src, dst, off, flag, timed=False, guard=None):
         works = exchange_halo(src, off, self.group, async_op=True)
         ev = self.kernel_events if timed else None
         L = self.local
         # interior cell planes first (they do not read the ghost plane) ...
         if off == 0:
-            self._launch(src, dst, off, 0, L - 1, flag, ev)
+            self._launch(src, dst, off, 0, L - 1, flag, ev, guard)
         else:
-            self._launch(src, dst, off, 1, L, flag, ev)
+            self._launch(src, dst, off, 1, L, flag, ev, guard)
         for w in works:
             w.wait()  # current stream waits for the NCCL stream
         # ... then the boundary cell plane that does
         if off == 0:
-            self._launch(src, dst, off, L - 1, L, flag, None)
+            self._launch(src, dst, off, L - 1, L, flag, None, guard)
         else:
-            self._launch(src, dst, off, 0, 1, flag, None)
+            self._launch(src, dst, off, 0, 1, flag, None, guard)
 
     def step(self, timed=False) -> None:
+        """One full step.  Guard chain (as `run_steps`): the first half step is skipped when the
+        previous step failed, the second when the first failed on any rank; flags are sticky, so
+        after an instability the solver stops changing the fields until `clear_flags()`."""
         if self.halo == "auto":
             raise RuntimeError("call init() first (it selects the halo path)")
+        f0, f1 = self.flags[0:1], self.flags[1:2]
         if self.halo == "p2p":
-            self._half_p2p(0, 1, 0, self.flags[0:1], timed)
-            self._half_p2p(1, 0, -1, self.flags[1:2], timed)
+            self._half_p2p(0, 1, 0, f0, timed, guard=f1)
+            self._half_p2p(1, 0, -1, f1, timed, guard=f0, collective_guard=True)
             return
-        self.half_step(self.bufs[0], self.bufs[1], 0, self.flags[0:1], timed)
-        self.half_step(self.bufs[1], self.bufs[0], -1, self.flags[1:2], timed)
+        self.half_step(self.bufs[0], self.bufs[1], 0, f0, timed, guard=f1)
+        self.half_step(self.bufs[1], self.bufs[0], -1, f1, timed, guard=self._any_bad(f0))
+
+    def clear_flags(self) -> None:
+        """Forget a reported instability (e.g. to retry from the untouched state with another dt)."""
+        self.flags.fill_(-1)
 
     def check(self, step_index=None) -> None:
         """Raise InstabilityError on EVERY rank when any rank has produced a non-finite value

@@ -459,11 +459,21 @@ def run_steps(
                      [first_step + k // 2 for k in range(2 * steps)])
 
 
-# captured step blocks, keyed by (field addresses and shapes, config, dt, block length): a graph
-# replays its kernels with the field pointers baked in, so it is valid for whatever tensors occupy
-# those addresses with those shapes.  Small LRU (the graphs hold no field references).
+# captured step blocks, keyed by (field addresses, shapes and dtype, config, dt, block length and
+# the bytes of every operator the kernels receive): a graph replays its kernels with the field
+# pointers and the launch parameters (H, the 1/h_k factors, the stage factors) baked in, so it is
+# valid for whatever tensors occupy those addresses with that shape and dtype AND the same
+# operators -- two grids with equal cells but different domain lengths (same dt) must not share
+# it.  Small LRU (the graphs hold no field references).
 _GRAPHS: "OrderedDict" = None
 _GRAPH_CACHE_SIZE = 16
+
+
+def _operator_key(ops: OperatorSet, dtype, dt: float, cfg: StepConfig) -> bytes:
+    """The exact launch parameters of a half step with these operators (their bytes)."""
+    np_dtype = np.float64 if dtype == torch.float64 else np.float32
+    arrays = _factor_arrays(ops, np_dtype, dt / 2, cfg.stages(ops.order_n))
+    return b"".join(np.ascontiguousarray(a).tobytes() for a in arrays)
 
 
 def _run_steps_graph(state, scratch, cfg, ops, steps, dt, first_step, block: int = 32) -> None:
@@ -474,8 +484,8 @@ def _run_steps_graph(state, scratch, cfg, ops, steps, dt, first_step, block: int
     done = 0
     while done < steps:
         nb = min(block, steps - done)
-        key = (state.tensor.data_ptr(), scratch.tensor.data_ptr(), tuple(state.tensor.shape), cfg, ops.order_n,
-               float(dt), nb, dev.index)
+        key = (state.tensor.data_ptr(), scratch.tensor.data_ptr(), tuple(state.tensor.shape), state.tensor.dtype,
+               cfg, ops.order_n, float(dt), nb, dev.index, _operator_key(ops, state.tensor.dtype, dt, cfg))
         global _GRAPHS
         if _GRAPHS is None:
             _GRAPHS = OrderedDict()

@@ -131,14 +131,18 @@ def build_ic(cfg: RunConfig) -> SeparableIC:
     return SeparableIC(terms=tuple(terms))
 
 
-def _plan_steps(cfg: RunConfig, grid: GridSpec, step_cfg: StepConfig) -> tuple[int, float]:
+def _plan_steps(cfg: RunConfig, grid: GridSpec, step_cfg: StepConfig, t0: float = 0.0) -> tuple[int, float]:
     """(full steps, dt).  A step count runs at the CFL dt; a final time is reached exactly by
     the fewest equal steps not exceeding the CFL dt (a 1e-12 slack absorbs T / dt rounding
-    just above an integer) -- the reference runner's plan (runner.py:65-76)."""
+    just above an integer) -- the reference runner's plan (runner.py:65-76).  A resumed run
+    (t0 > 0, an extension of the reference) plans the remaining interval final_time - t0."""
     cfl_dt = select_dt(grid, step_cfg)
     if cfg.steps is None:
-        count = max(1, math.ceil(cfg.final_time / cfl_dt - 1e-12))
-        return count, cfg.final_time / count
+        span = cfg.final_time - t0
+        if not span > 0:
+            raise ConfigError(f"final_time: {cfg.final_time} is not after the resumed snapshot time {t0}")
+        count = max(1, math.ceil(span / cfl_dt - 1e-12))
+        return count, span / count
     return cfg.steps, cfl_dt
 
 
@@ -218,8 +222,10 @@ def execute_run(cfg: RunConfig, write_artifacts: bool = True) -> dict:
     else:
         state = init_field(ic, grid, cfg.order_n, precision=cfg.precision)
     scratch = DofField.zeros(grid.with_parity("dual"), cfg.order_n, precision=cfg.precision)
-    n_steps, dt = _plan_steps(cfg, grid, step_cfg)
-    track = ic.smoothness_class == "analytic" and cfg.precision == "double"
+    n_steps, dt = _plan_steps(cfg, grid, step_cfg, t0)
+    # errors are tracked for every precision, as the reference does (runner.py:156); the device
+    # reduction upcasts single-precision DOFs to FP64
+    track = ic.smoothness_class == "analytic"
     stats = AllocationStats()
     dev = state.device
     norms = torch.zeros((n_steps + 1, 2), dtype=torch.float64, device=dev)

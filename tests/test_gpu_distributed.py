@@ -111,14 +111,20 @@ def _bad_worker(rank, world, port, cells, bad, halo, result_path):
         solver.init(hb.plane_wave())
         if solver.z0 <= bad[0] < solver.z1:
             solver.state[(bad[0] - solver.z0,) + tuple(bad[1:])] = float("inf")
+        before = solver.state.clone()
         err = None
         try:
             solver.step()
             solver.check(step_index=4)
         except hb.InstabilityError as e:
             err = (e.node, e.step)
+        # the reference raises after the first half step with the state untouched: the second
+        # half step is skipped on EVERY rank (collective guard), and so is any later step
+        untouched = torch.equal(solver.state, before)
+        solver.step()
+        untouched = untouched and torch.equal(solver.state, before)
         errs = [None] * world
-        dist.all_gather_object(errs, err)
+        dist.all_gather_object(errs, (err, untouched))
         if rank == 0:
             grid = hb.GridSpec(cells)
             state = hb.init_field(hb.plane_wave(), grid, 3)
@@ -128,7 +134,7 @@ def _bad_worker(rank, world, port, cells, bad, halo, result_path):
                 hb.full_step(state, scratch, cfg, hb.OperatorSet.for_grid(grid, 3), dt=solver.dt, step_index=4)
             want = (ref.value.node, ref.value.step)
             with open(result_path, "w") as fh:
-                fh.write("ok" if all(e == want for e in errs) else f"mismatch {errs} vs {want}")
+                fh.write("ok" if all(e == (want, True) for e in errs) else f"mismatch {errs} vs {want}")
         dist.barrier()
         solver.close()
     finally:

@@ -491,6 +491,45 @@ def test_run_steps_graph_replay_bitwise(order_n, cells, steps):
     assert torch.equal(outs[0], outs[1])
 
 
+def test_separable_accepts_any_exact_stage_count():
+    """The reference accepts any stages_q >= 1; the separable path (exact for q >= 3(2N+1))
+    gives the same field for q = 200 as for the default q (only the literal kernels cap q)."""
+    grid = hb.GridSpec((9, 8, 7))
+    ops = hb.OperatorSet.for_grid(grid, 3)
+    outs = []
+    for q in (None, 200):
+        st = hb.init_field(hb.plane_wave(), grid, 3)
+        sc = hb.DofField.zeros(grid.with_parity("dual"), 3)
+        hb.full_step(st, sc, hb.StepConfig(stages_q=q), ops)
+        outs.append(st.tensor.clone())
+    assert torch.equal(outs[0], outs[1])
+
+
+def test_run_steps_graph_cache_distinguishes_operators():
+    """Two grids with equal cells and equal dt (the minimal spacing is the same) but different
+    domain lengths along another axis, stepped on fields at the SAME device addresses: the
+    second run must not replay the first grid's captured operators."""
+    order_n, steps = 3, 9
+    ga = hb.GridSpec((12, 10, 9), (1.0, 1.0, 1.0))
+    gb = hb.GridSpec((12, 10, 9), (1.0, 1.5, 1.0))
+    cfg = hb.StepConfig(variant="separable")
+    dt = hb.select_dt(ga, cfg)
+    assert dt == hb.select_dt(gb, cfg)
+    st = hb.init_field(hb.plane_wave(), ga, order_n)
+    sc = hb.DofField.zeros(ga.with_parity("dual"), order_n)
+    init = st.tensor.clone()
+    hb.run_steps(st, sc, cfg, hb.OperatorSet.for_grid(ga, order_n), steps, dt=dt, graph=True)
+    st.tensor.copy_(init)
+    stb = hb.DofField(gb, order_n, st.tensor)             # same storage, other grid
+    scb = hb.DofField(gb.with_parity("dual"), order_n, sc.tensor)
+    hb.run_steps(stb, scb, cfg, hb.OperatorSet.for_grid(gb, order_n), steps, dt=dt, graph=True)
+    got = stb.tensor.clone()
+    ref = hb.DofField(gb, order_n, init.clone())
+    refs = hb.DofField.zeros(gb.with_parity("dual"), order_n)
+    hb.run_steps(ref, refs, cfg, hb.OperatorSet.for_grid(gb, order_n), steps, dt=dt, graph=False)
+    assert torch.equal(got, ref.tensor)
+
+
 def test_run_steps_graph_reports_instability_step():
     grid = hb.GridSpec((8, 7, 6))
     cfg = hb.StepConfig(variant="separable")
