@@ -144,6 +144,48 @@ int h3_error_norms(const double* field, int64_t M1, int64_t M2, int64_t M3, int 
 int h3_check_finite(const double* field, int64_t M1, int64_t M2, int64_t M3, int order_n,
                     unsigned long long* d_first_bad, void* stream);
 
+/* ---- per-cell API (reference kernels.py:73-191, the numpy per-cell API) -------------------
+ * A batch of `batch` cells, each an (n3, n2, n1) tensor stored contiguously [n3][n2][n1];
+ * every pointer is DEVICE memory of the precision `single` selects (1: float, 0: double).
+ * The arithmetic is the reference's numpy arithmetic (separate multiplies and adds, same
+ * order, same typed zeros), so results are bit-identical to it.  fac_k: per-axis factors
+ * (i+1)*(1/h_k) rounded to the precision, length n_k (last entry unused), as
+ * kernels.py:90-96 forms them. */
+
+/* One sweep of reconstruct_cell (kernels.py:80-86) = operators.apply_along_axis(H, u, axis)
+ * (operators.py:127-151): out = sum_k mat[i][k] x[k] along `axis` (1 = x1 = last index),
+ * accumulated from zero in ascending k; mat is [len][len] of that axis. */
+int h3_cell_apply_axis(const void* in, void* out, int64_t batch, int n3, int n2, int n1,
+                       const void* mat, int axis, int single, void* stream);
+
+/* advect_time_derivative (kernels.py:99-108). */
+int h3_cell_advect(const void* w, void* out, int64_t batch, int n3, int n2, int n1,
+                   const void* fac1, const void* fac2, const void* fac3, int single, void* stream);
+
+/* taylor_evolve_horner (kernels.py:111-128): q stages, cstage[k-1] = step / k in the
+ * precision; `tmp` is scratch of the same size as `out`. */
+int h3_cell_horner(const void* b, void* out, void* tmp, int64_t batch, int n3, int n2, int n1,
+                   const void* fac1, const void* fac2, const void* fac3, const void* cstage,
+                   int q, int single, void* stream);
+
+/* space_time_tensor (kernels.py:131-142): st[cell][j][...], j = 0..q, cstage[j] = dt/(j+1). */
+int h3_cell_space_time(const void* b, void* st, int64_t batch, int n3, int n2, int n1,
+                       const void* fac1, const void* fac2, const void* fac3, const void* cstage,
+                       int q, int single, void* stream);
+
+/* The sum of taylor_evolve_recursion (kernels.py:157-164): out = st[0] + st[1] t_1 + ...,
+ * accumulated in ascending j; tpow[j-1] = tau^j (repeated products, rounded once). */
+int h3_cell_time_sum(const void* st, void* out, int64_t batch, int64_t size, const void* tpow,
+                     int q, int single, void* stream);
+
+/* verify_space_time_identity (kernels.py:167-191): *d_worst (a double's bits, atomically
+ * max-reduced; initialise to 0) = max over j, entries of |coef[j] st[j+1] - L st[j]|
+ * (j < q) and |L st[q]|, coef[j] = (j+1)/dt in the precision. */
+int h3_cell_identity_residual(const void* st, int64_t batch, int n3, int n2, int n1,
+                              const void* fac1, const void* fac2, const void* fac3,
+                              const void* coef, int q, unsigned long long* d_worst, int single,
+                              void* stream);
+
 const char* h3_version(void);
 const char* h3_error_string(int status);
 int h3_max_order(void);

@@ -43,6 +43,13 @@ SIGNATURES = {
     "h3_ipc_export": (_i32, [_vp, _vp, _vp]),
     "h3_ipc_open": (_i32, [_vp, _vp]),
     "h3_ipc_close": (_i32, [_vp]),
+    "h3_cell_apply_axis": (_i32, [_vp, _vp, _i64, _i32, _i32, _i32, _vp, _i32, _i32, _vp]),
+    "h3_cell_advect": (_i32, [_vp, _vp, _i64, _i32, _i32, _i32, _vp, _vp, _vp, _i32, _vp]),
+    "h3_cell_horner": (_i32, [_vp, _vp, _vp, _i64, _i32, _i32, _i32, _vp, _vp, _vp, _vp, _i32, _i32, _vp]),
+    "h3_cell_space_time": (_i32, [_vp, _vp, _i64, _i32, _i32, _i32, _vp, _vp, _vp, _vp, _i32, _i32, _vp]),
+    "h3_cell_time_sum": (_i32, [_vp, _vp, _i64, _i64, _vp, _i32, _i32, _vp]),
+    "h3_cell_identity_residual": (_i32, [_vp, _i64, _i32, _i32, _i32, _vp, _vp, _vp, _vp, _i32, _u64p, _i32,
+                                         _vp]),
     "h3_version": (ctypes.c_char_p, []),
     "h3_error_string": (ctypes.c_char_p, [_i32]),
     "h3_max_order": (_i32, []),
@@ -63,15 +70,29 @@ def build(verbose: bool = False) -> Path:
     return LIB_PATH
 
 
+_LIB_OVERRIDE: Path | None = None
+
+
+def use_library(path) -> None:
+    """Bind a different build of the same C ABI before first use -- for the measurement tools,
+    which load build/libh3b200_measure.so (`make -C csrc measure`: the same kernels plus
+    measurement-only variants).  The product never calls this."""
+    global _LIB_OVERRIDE
+    if lib.cache_info().currsize:
+        raise NativeLibraryError("use_library() must be called before the library is first used")
+    _LIB_OVERRIDE = Path(path)
+
+
 @lru_cache(maxsize=None)
 def lib() -> ctypes.CDLL:
-    if not LIB_PATH.exists():
+    path = _LIB_OVERRIDE or LIB_PATH
+    if not path.exists():
         raise NativeLibraryError(
-            f"{LIB_PATH} not found; build it with `make -C {CSRC}` or __graft_entry__.build()")
+            f"{path} not found; build it with `make -C {CSRC}` or __graft_entry__.build()")
     try:
-        so = ctypes.CDLL(str(LIB_PATH))
+        so = ctypes.CDLL(str(path))
     except OSError as exc:
-        raise NativeLibraryError(f"failed to load {LIB_PATH}: {exc}") from exc
+        raise NativeLibraryError(f"failed to load {path}: {exc}") from exc
     for name, (res, args) in SIGNATURES.items():
         fn = getattr(so, name)
         fn.restype = res

@@ -117,13 +117,17 @@ static int recon_impl(const T* src, T* coeff, int64_t M1, int64_t M2, int64_t M3
     Dims d{M1, M2, M3, z_begin, z_end, periodic_z ? 1 : 0};
     if (fast && sizeof(T) == 8) {
         // node-factorised reconstruction: FP64 tensor cores at N = 3 and 5, DFMA otherwise
-        // (H3_RECON_IMPL=sep: DFMA kernel at N = 3 too; =fma: per-cell sweeps, for A/B runs)
+#ifdef H3_MEASURE
+        // tools library only (H3_RECON_IMPL=sep: DFMA kernel at N = 3 too; =fma: per-cell sweeps)
         static const int impl = [] {
             const char* e = getenv("H3_RECON_IMPL");
             if (e && strcmp(e, "fma") == 0) return 2;
             if (e && strcmp(e, "sep") == 0) return 1;
             return 0;
         }();
+#else
+        constexpr int impl = 0;
+#endif
         cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
         if (impl == 0 && order_n == 3)
             return h3::recon_dmma3_launch((const double*)src, (double*)coeff, d, (const double*)h_mat, off, st,

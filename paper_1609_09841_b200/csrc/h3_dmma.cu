@@ -467,13 +467,17 @@ static int launch_dm3(const double* src, double* dst, const Dims& d, const SepOp
     const int64_t gx = (d.M1 + C::TX - 1) / C::TX, gy = (d.M2 + C::TY - 1) / C::TY;
     const int64_t zchunk = choose_zchunk(gx * gy, nz, (int64_t)num_sms() * (per_sm > 0 ? per_sm : 1));
     const int64_t gz = (nz + zchunk - 1) / zchunk;
-    // Thread-block clusters of 2 tiles along x2 (H3_DMMA_CLUSTER_Y, 1 = off): y-adjacent tiles
-    // share a node row; co-scheduling them keeps that row in L2 for the second reader
-    // (DRAM over-read 14% -> measured +4.5% throughput at 512^3).
-    static const int cy = [] {
+    // Thread-block clusters of 2 tiles along x2: y-adjacent tiles share a node row;
+    // co-scheduling them keeps that row in L2 for the second reader (DRAM over-read 14% ->
+    // measured +4.5% throughput at 512^3).
+#ifdef H3_MEASURE
+    static const int cy = [] {  // tools library only: H3_DMMA_CLUSTER_Y (1 = off)
         const char* e = getenv("H3_DMMA_CLUSTER_Y");
         return e ? atoi(e) : 2;
     }();
+#else
+    constexpr int cy = 2;
+#endif
     if (cy > 1 && gy % cy == 0) {
         cudaLaunchConfig_t lc = {};
         lc.gridDim = dim3((unsigned)gx, (unsigned)gy, (unsigned)gz);
@@ -508,23 +512,26 @@ int sep_fused_dmma3_launch(const double* src, double* dst, const Dims& d, const 
                 ops.A[k][m][c] = A[(k * 4 + m) * 8 + c];
                 ops.Sh[k][m][c] = 0.0;
             }
-    // tile configuration (H3_DMMA_CFG selects alternatives for measurements)
+#ifdef H3_MEASURE
+    // tools library only: H3_DMMA_CFG=k selects the measurement variants of tools/ab.sh
+    // (ablations 11/14/15 skip stores / replace the DMMAs and produce garbage on purpose)
     static const int cfg = [] {
         const char* e = getenv("H3_DMMA_CFG");
         return e ? atoi(e) : 0;
     }();
     switch (cfg) {
-        // measurement variants (tools/time_fused.py with H3_DMMA_CFG=k)
         case 6: return launch_dm3<Dm3Cfg<7, 16, 3, true>>(src, dst, d, ops, off, st, first_bad, guard);  // cp.async loads
         case 11: return launch_dm3<Dm3Cfg<7, 16, 3, true, 1, 1, true>>(src, dst, d, ops, off, st, first_bad, guard);
         case 14: return launch_dm3<Dm3Cfg<7, 16, 3, true, 1, 4, true>>(src, dst, d, ops, off, st, first_bad, guard);
         case 15: return launch_dm3<Dm3Cfg<7, 16, 3, true, 1, 5, true>>(src, dst, d, ops, off, st, first_bad, guard);
         case 16: return launch_dm3<Dm3Cfg<7, 16, 3, true, 1, 0, true>>(src, dst, d, ops, off, st, first_bad, guard);
         case 31: return launch_dm3<Dm3Cfg<7, 16, 3, false, 1, 0, true, true, 1, false>>(src, dst, d, ops, off, st, first_bad, guard);  // bank-conflicted W/V
-        // default: TMA row loads, x3(p-1) pipelined with x1(p) (2 barriers per plane), lean x3 stores,
-        // conflict-free W / V strides
-        default: return launch_dm3<Dm3Cfg<7, 16, 3, false, 1, 0, true, true, 1, true>>(src, dst, d, ops, off, st, first_bad, guard);
+        default: break;
     }
+#endif
+    // TMA row loads, x3(p-1) pipelined with x1(p) (2 barriers per plane), lean x3 stores,
+    // conflict-free W / V strides
+    return launch_dm3<Dm3Cfg<7, 16, 3, false, 1, 0, true, true, 1, true>>(src, dst, d, ops, off, st, first_bad, guard);
 }
 
 

@@ -308,12 +308,14 @@ static int launch_cp(const double* src, double* dst, const Dims& d, const double
 
 int sep_fused_dmma5_launch(const double* src, double* dst, const Dims& d, const double* A, int off, cudaStream_t st,
                            unsigned long long* first_bad, const unsigned long long* guard) {
-    static const int cfg = [] {
+#ifdef H3_MEASURE
+    static const int cfg = [] {  // tools library only: alternative tile shapes for tools/ab.sh
         const char* e = getenv("H3_DMMA5_CFG");
         return e ? atoi(e) : 0;
     }();
     if (cfg == 1) return launch_cp<cp5::Cfg<5, 4, 2, 8, 2, 2>>(src, dst, d, A, off, st, first_bad, guard);
     if (cfg == 2) return launch_cp<cp5::Cfg<5, 4, 2, 8, 3, 1>>(src, dst, d, A, off, st, first_bad, guard);
+#endif
     return launch_cp<cp5::Cfg<5, 4, 4>>(src, dst, d, A, off, st, first_bad, guard);
 }
 

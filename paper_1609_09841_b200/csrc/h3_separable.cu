@@ -267,6 +267,20 @@ static int sep_fused_n(const double* src, double* dst, const Dims& d, const doub
     return (int)cudaGetLastError();
 }
 
+// H3_FUSED_IMPL=dfma runs the DFMA kernel at N = 3, 5 too: only in the tools library
+// (-DH3_MEASURE), which backs the "DMMA only where ncu shows compute-bound" comparison.
+static bool use_dfma_ab() {
+#ifdef H3_MEASURE
+    static const bool v = [] {
+        const char* e = getenv("H3_FUSED_IMPL");
+        return e && strcmp(e, "dfma") == 0;
+    }();
+    return v;
+#else
+    return false;
+#endif
+}
+
 int sep_fused_launch(const double* src, double* dst, const Dims& d, int order_n, const double* A,
                      int off, cudaStream_t st, unsigned long long* first_bad,
                      const unsigned long long* guard) {
@@ -274,26 +288,15 @@ int sep_fused_launch(const double* src, double* dst, const Dims& d, int order_n,
         case 0: return sep_fused_n<0>(src, dst, d, A, off, st, first_bad, guard);
         case 1: return sep_fused_n<1>(src, dst, d, A, off, st, first_bad, guard);
         case 2: return sep_fused_n<2>(src, dst, d, A, off, st, first_bad, guard);
-        case 3: {
-            // FP64 tensor-core kernel (h3_dmma.cu) unless H3_FUSED_IMPL=dfma asks for the
-            // DFMA kernel (kept for A/B measurements).
-            static const bool use_dfma = [] {
-                const char* e = getenv("H3_FUSED_IMPL");
-                return e && strcmp(e, "dfma") == 0;
-            }();
-            if (use_dfma) return sep_fused_n<3>(src, dst, d, A, off, st, first_bad, guard);
+        case 3:
+            // FP64 tensor-core kernel (h3_dmma.cu); the DFMA kernel is the tools library's A/B
+            if (use_dfma_ab()) return sep_fused_n<3>(src, dst, d, A, off, st, first_bad, guard);
             return sep_fused_dmma3_launch(src, dst, d, A, off, st, first_bad, guard);
-        }
         case 4: return sep_fused_n<4>(src, dst, d, A, off, st, first_bad, guard);
-        case 5: {
-            // FP64 tensor-core cell-pair kernel (h3_dmma5.cu) unless H3_FUSED_IMPL=dfma
-            static const bool use_dfma = [] {
-                const char* e = getenv("H3_FUSED_IMPL");
-                return e && strcmp(e, "dfma") == 0;
-            }();
-            if (use_dfma) return sep_fused_n<5>(src, dst, d, A, off, st, first_bad, guard);
+        case 5:
+            // FP64 tensor-core cell-pair kernel (h3_dmma5.cu)
+            if (use_dfma_ab()) return sep_fused_n<5>(src, dst, d, A, off, st, first_bad, guard);
             return sep_fused_dmma5_launch(src, dst, d, A, off, st, first_bad, guard);
-        }
     }
     return (int)cudaErrorInvalidValue;
 }
@@ -436,7 +439,8 @@ static int sep_evolve_n(const double* coeff, double* dst, const Dims& d, const d
                         cudaStream_t st, unsigned long long* first_bad,
                         const unsigned long long* guard) {
     if constexpr (N == 3) {
-        static const int cpb = [] {
+#ifdef H3_MEASURE
+        static const int cpb = [] {  // tools library only: cells per CTA for A/B runs
             const char* e = getenv("H3_EVOLVE_CPB");
             return e ? atoi(e) : 0;
         }();
@@ -444,6 +448,7 @@ static int sep_evolve_n(const double* coeff, double* dst, const Dims& d, const d
         if (cpb == 2) return sep_evolve_nc<3, 2>(coeff, dst, d, Sh, st, first_bad, guard);
         if (cpb == 42) return sep_evolve_nc<3, 4, 2>(coeff, dst, d, Sh, st, first_bad, guard);
         if (cpb == 8) return sep_evolve_nc<3, 8>(coeff, dst, d, Sh, st, first_bad, guard);
+#endif
         // one cell (64 threads) per CTA: 32 independent CTAs per SM overlap their load and
         // contraction phases best (measured 4.7 vs 4.2 TB/s for 2-8 cells per CTA)
         return sep_evolve_nc<3, 1>(coeff, dst, d, Sh, st, first_bad, guard);

@@ -148,13 +148,18 @@ class SlabSolver:
         q = cfg.stages(order_n)
         self._fac = _factor_arrays(self.ops, np.float64, self.dt / 2, q)
         self._q = q
-        if cfg.mode != "fused":
-            raise NotImplementedError("SlabSolver runs the fused half step")
         if halo not in ("nccl", "p2p", "auto"):
             raise ValueError(f"halo must be 'nccl', 'p2p' or 'auto', got {halo!r}")
         self.halo = halo
         self.halo_note = ""
-        if halo == "auto":
+        self._coeff = None  # two-pass coefficient chunk (allocated at the first half step)
+        if cfg.mode == "two_pass":
+            # the in-kernel p2p halo exists for the monolithic kernels; the two-kernel step reads
+            # its ghost plane from the NCCL copy (recon_pass with periodic_z = 0)
+            if halo == "p2p":
+                raise ValueError("the p2p halo is implemented for the fused mode; use halo='nccl'")
+            self.halo, self.halo_note = "nccl", ("two-kernel step: NCCL halo" if halo == "auto" else "")
+        elif halo == "auto":
             # in-kernel p2p halo where it is available (N = 3, 5), verified against the NCCL copy
             # on the first initialised field (init); any failure falls back to NCCL
             if order_n in (3, 5):
@@ -168,8 +173,17 @@ class SlabSolver:
     @property
     def launches_per_step(self) -> int:
         """Kernel launches per full step: one per half step with the in-kernel halo, two (interior
-        + boundary plane) with the NCCL copy."""
+        + boundary plane) with the NCCL copy; the two-kernel step launches recon + evolve per
+        coefficient chunk of each range."""
+        if self.cfg.mode == "two_pass":
+            chunk = self._coeff_planes()
+            return 2 * 2 * (-(-(self.local - 1) // chunk) + 1)
         return 2 if self.halo == "p2p" else 4
+
+    def _coeff_planes(self) -> int:
+        from .pipeline import _coeff_chunk_planes
+        m1, m2, _ = self.grid.cells_per_axis
+        return _coeff_chunk_planes(GridSpec((m1, m2, self.local)), self.order_n, 8, self.cfg.coeff_budget_bytes)
 
     @property
     def state(self) -> torch.Tensor:
@@ -236,6 +250,13 @@ class SlabSolver:
         e0 = torch.cuda.Event(enable_timing=True) if events is not None else None
         if e0 is not None:
             e0.record(stream)
+        if self.cfg.mode == "two_pass":
+            self._launch_two_pass(src, dst, off, zb, ze, flag, guard, plane, stream)
+            if e0 is not None:
+                e1 = torch.cuda.Event(enable_timing=True)
+                e1.record(stream)
+                events.append((e0, e1))
+            return
         rc = _native.lib().h3_fused_pass(
             ctypes.c_void_p(src.data_ptr() + plane), ctypes.c_void_p(dst.data_ptr() + plane),
             m1, m2, self.local, self.order_n, _ptr(h_mat), _ptr(f1), _ptr(f2), _ptr(f3), _ptr(cf),
@@ -246,6 +267,29 @@ class SlabSolver:
             e1 = torch.cuda.Event(enable_timing=True)
             e1.record(stream)
             events.append((e0, e1))
+
+    def _launch_two_pass(self, src, dst, off, zb, ze, flag, guard, plane, stream):
+        """The two-kernel half step of cells [zb, ze) of the slab (reference pipeline.py:254-273):
+        reconstruction into a coefficient chunk -- reading the ghost plane at the slab edge
+        (periodic_z = 0) -- then evolution, chunk by chunk."""
+        m1, m2, _ = self.grid.cells_per_axis
+        s = 2 * self.order_n + 2
+        if self._coeff is None:
+            self._coeff = torch.empty((self._coeff_planes(), m2, m1, s, s, s), dtype=torch.float64, device="cuda")
+        h_mat, f1, f2, f3, cf = self._fac
+        lib, var = _native.lib(), _native.VARIANTS[self.cfg.variant]
+        sp, dp = ctypes.c_void_p(src.data_ptr() + plane), ctypes.c_void_p(dst.data_ptr() + plane)
+        cp = ctypes.c_void_p(self._coeff.data_ptr())
+        sh = ctypes.c_void_p(stream.cuda_stream)
+        gp = None if guard is None else ctypes.c_void_p(guard.data_ptr())
+        chunk = self._coeff.shape[0]
+        for z0 in range(zb, ze, chunk):
+            z1 = min(ze, z0 + chunk)
+            _native.check(lib.h3_recon_pass(sp, cp, m1, m2, self.local, self.order_n, _ptr(h_mat), off, z0, z1, 0,
+                                            var, sh, gp), "h3_recon_pass (slab)")
+            _native.check(lib.h3_evolve_pass(cp, dp, m1, m2, self.local, self.order_n, _ptr(f1), _ptr(f2), _ptr(f3),
+                                             _ptr(cf), self._q, z0, z1, var, sh, ctypes.c_void_p(flag.data_ptr()),
+                                             gp), "h3_evolve_pass (slab)")
 
     # ---- p2p halo: the kernel reads the neighbour's boundary plane in place (CUDA IPC / NVLink) ----
     def _all_ranks_ok(self, ok: bool) -> bool:

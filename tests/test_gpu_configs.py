@@ -1,0 +1,128 @@
+"""Parity and convergence at the BASELINE.json configuration sizes themselves.
+
+* configs[3] (m=5, 256^3, two-kernel vs monolithic, convergence vs the exact plane wave):
+  128^3 -> 256^3 at k=40 (3.2 points per wavelength on the coarse grid), final time 0.1, both
+  modes.  The observed L_inf order must reach 2N+0.5 = 10.5 (the reference's
+  execute_converge, runner.py:203-236), and the errors must agree with the reference's own
+  run of the scale-equivalent problem (tests/golden/conv5.json).  Fused and two-kernel are
+  compared over the whole 256^3 run.
+* configs[1] (m=3, 128^3, two-kernel): the separable path vs the literal path (the
+  reference's arithmetic, bit-identical to it) over 3 full steps, both modes, <= 1e-11.
+* configs[2] (m=3, 512^3): the separable fused and two-kernel steps vs the literal step over
+  2 full steps at the full size.  The literal result (68.7 GB) is staged through host memory
+  and compared chunk by chunk, <= 1e-11 (the north star's parity bound).
+
+Errors are the reference's normwise metric (pkg/tests/conftest.py:27-32 rel_err: max |diff|
+over max |reference|), reduced on the device in x3 chunks (no whole-field temporaries).
+"""
+
+import json
+import math
+from pathlib import Path
+
+import pytest
+import torch
+
+import paper_1609_09841_b200 as hb
+
+pytestmark = pytest.mark.gpu
+
+CONV5 = json.loads((Path(__file__).parent / "golden" / "conv5.json").read_text())
+
+
+def _chunked_rel_err(got: torch.Tensor, want: torch.Tensor, planes: int = 8) -> float:
+    """max |got - want| / max |want| over x3 chunks; `want` may live in host memory."""
+    num = den = 0.0
+    for z0 in range(0, got.shape[0], planes):
+        z1 = min(z0 + planes, got.shape[0])
+        w = want[z0:z1].to(got.device, non_blocking=True)
+        num = max(num, float((got[z0:z1] - w).abs().max()))
+        den = max(den, float(w.abs().max()))
+    return num / (den if den > 0 else 1.0)
+
+
+def _run(grid, order_n, cfg, ic, steps, dt, graph=False):
+    state = hb.init_field(ic, grid, order_n)
+    scratch = hb.DofField.empty(grid.with_parity("dual"), order_n)
+    hb.run_steps(state, scratch, cfg, hb.OperatorSet.for_grid(grid, order_n), steps, dt=dt, graph=graph)
+    del scratch
+    return state
+
+
+def test_configs3_m5_convergence_128_to_256_both_modes():
+    order_n, k, final_time = 5, CONV5["scaled_to"]["wavenumber"], CONV5["scaled_to"]["final_time"]
+    ic = hb.plane_wave(k)
+    errors = {}
+    finals = {}
+    for mode in ("fused", "two_pass"):
+        cfg = hb.StepConfig(mode=mode, variant="separable")
+        errs = []
+        for m, ref in zip(CONV5["scaled_to"]["cells"], CONV5["rows"]):
+            grid = hb.GridSpec((m, m, m))
+            steps = max(1, math.ceil(final_time / hb.select_dt(grid, cfg) - 1e-12))
+            assert steps == ref["steps"]  # the scale-equivalent problem of the reference's run
+            state = _run(grid, order_n, cfg, ic, steps, final_time / steps)
+            err = hb.compute_error(state, hb.exact_solution(ic, final_time))
+            errs.append(err.l_inf)
+            # the reference's error on the scale-equivalent problem (same DOFs up to rounding)
+            assert err.l_inf == pytest.approx(ref["l_inf"], rel=0.02)
+            assert err.l2 == pytest.approx(ref["l2"], rel=0.02)
+            if m == 256:
+                finals[mode] = state.tensor
+            del state
+        order = math.log2(errs[0] / errs[1])
+        assert order >= 2 * order_n + 0.5, (mode, errs, order)
+        errors[mode] = (errs, order)
+    gap = _chunked_rel_err(finals["two_pass"], finals["fused"])
+    print(f"configs[3]: errors/orders {errors}; fused vs two-pass at 256^3 after the run: {gap:.3e}")
+    assert gap <= 1e-9
+
+
+@pytest.mark.parametrize("mode", ["two_pass", "fused"])
+def test_configs1_m3_128_separable_vs_literal(mode):
+    grid = hb.GridSpec((128, 128, 128))
+    rng_terms = []
+    import numpy as np
+    rng = np.random.default_rng(11)
+    for _ in range(4):
+        rng_terms.append(tuple(hb.FourierMode(float(rng.uniform(-1, 1)), int(rng.integers(1, 4)),
+                                              float(rng.uniform(0, 2 * np.pi))) for _ in range(3)))
+    ic = hb.SeparableIC(tuple(rng_terms))
+    dt = hb.select_dt(grid, hb.StepConfig())
+    lit = _run(grid, 3, hb.StepConfig(mode=mode, variant="literal"), ic, 3, dt).tensor
+    sep = _run(grid, 3, hb.StepConfig(mode=mode, variant="separable"), ic, 3, dt).tensor
+    err = _chunked_rel_err(sep, lit)
+    print(f"configs[1] {mode}: separable vs literal after 3 steps at 128^3: {err:.3e}")
+    assert err <= 1e-11
+
+
+def _host_gb_free() -> float:
+    try:
+        import psutil
+        return psutil.virtual_memory().available / 1e9
+    except ImportError:  # pragma: no cover
+        return 0.0
+
+
+@pytest.mark.skipif(_host_gb_free() < 90, reason="needs ~70 GB of free host memory to stage the 512^3 field")
+def test_configs2_m3_512_full_size_separable_vs_literal():
+    """The headline size itself: 512^3 m=3 (8.6e9 DOFs, 68.7 GB per field), 2 full steps."""
+    grid = hb.GridSpec((512, 512, 512))
+    ic = hb.plane_wave()
+    dt = hb.select_dt(grid, hb.StepConfig())
+    lit = _run(grid, 3, hb.StepConfig(mode="fused", variant="literal"), ic, 2, dt)
+    try:
+        staged = torch.empty(lit.tensor.shape, dtype=torch.float64, pin_memory=True)
+    except RuntimeError:
+        staged = torch.empty(lit.tensor.shape, dtype=torch.float64)
+    staged.copy_(lit.tensor)
+    lit.release()
+    torch.cuda.empty_cache()
+    for mode in ("fused", "two_pass"):
+        sep = _run(grid, 3, hb.StepConfig(mode=mode, variant="separable"), ic, 2, dt)
+        assert sep.all_finite()
+        err = _chunked_rel_err(sep.tensor, staged)
+        print(f"configs[2] 512^3 {mode}: separable vs literal after 2 steps: {err:.3e}")
+        assert err <= 1e-11
+        sep.release()
+        torch.cuda.empty_cache()

@@ -237,3 +237,21 @@ def test_streaming_chunk_plan_covers_the_grid():
             assert all(z1 - z0 >= 2 for z0, z1 in plan)
     with pytest.raises(ValueError):
         chunk_plan(1, 4)
+
+
+def test_product_library_has_no_measurement_variants_or_environment_reads():
+    """The measurement-only kernel variants (ablations that skip stores or DMMAs, alternative
+    tiles, the DFMA A/B kernels) and every H3_* environment switch exist only in the tools build
+    (-DH3_MEASURE, build/libh3b200_measure.so): the product objects reference no getenv and the
+    product library holds one instantiation of the N=3 monolithic kernel, with no ablation bits."""
+    import subprocess
+    objs = sorted((ROOT / "build" / "obj").glob("*.o"))
+    assert objs
+    for o in objs:
+        syms = subprocess.run(["nm", str(o)], capture_output=True, text=True).stdout
+        assert " U getenv" not in syms, o
+    dump = subprocess.run(["cuobjdump", "-symbols", str(_native.LIB_PATH)], capture_output=True, text=True).stdout
+    fused3 = set(re.findall(r"sep_fused_dmma3_kernelINS_6Dm3CfgI(\w+?)EEEEEv", dump))
+    assert len(fused3) == 1, fused3
+    # template arguments <TY, WARPS, STAGES, VALIAS, MINB, ABL, ...>: ABL (the 6th) must be 0
+    assert re.match(r"Li7ELi16ELi3ELb0ELi1ELi0E", next(iter(fused3))), fused3

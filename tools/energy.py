@@ -14,6 +14,8 @@ import pynvml
 import torch
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import _lib  # noqa: E402
+_lib.select_library()
 import paper_1609_09841_b200 as hb  # noqa: E402
 
 m = int(sys.argv[1]) if len(sys.argv) > 1 else 512

@@ -5,6 +5,8 @@ import sys
 import torch
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import _lib  # noqa: E402
+_lib.select_library()
 import paper_1609_09841_b200 as hb  # noqa: E402
 
 n, m = int(sys.argv[1]), int(sys.argv[2])

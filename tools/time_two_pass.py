@@ -2,6 +2,8 @@
 import sys
 import torch
 sys.path.insert(0, ".")
+import _lib  # noqa: E402
+_lib.select_library()
 import paper_1609_09841_b200 as hb
 
 for n, m in [(3, 128), (3, 256), (1, 256), (5, 128)]:
