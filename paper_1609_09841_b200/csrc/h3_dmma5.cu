@@ -57,8 +57,11 @@ __device__ __forceinline__ bool live(int warp, int it) {
     return G % WARPS == 0 || warp + WARPS * it < G;
 }
 
-template <int N_, int TX_, int TY_, int WARPS_ = 16, int STAGES_ = 3, int MINB_ = 1>
+template <int N_, int TX_, int TY_, int WARPS_ = 16, int STAGES_ = 3, int MINB_ = 1, bool ILP_ = false>
 struct Cfg {
+    // ILP: issue a pass's DMMAs k-step-major (all line groups of the warp at k-step 0, then 1, 2),
+    // so consecutive DMMAs are independent, instead of one group's 3-deep accumulation chain
+    static constexpr bool ILP = ILP_;
     static constexpr int N = N_, n = N + 1, n2 = n * n, n3 = n2 * n, K2 = 2 * n;
     static constexpr int KS = K2 / 4;  // m8n8k4 k-steps per line
     static_assert(K2 % 4 == 0, "cell-pair form needs 2n divisible by 4");
@@ -219,12 +222,22 @@ sep_fused_dmma_cp_kernel(const double* __restrict__ src, double* __restrict__ ds
             for (int ks = 0; ks < KS; ++ks) vk[ks] = V + ((cp + ka[ks]) & 1) * C::V_D + k3[ks];
             double* oplane = dst + (zc0 + cp) * plane_elems;
             double d[I3][2];
+            if constexpr (C::ILP) {
+#pragma unroll
+                for (int it = 0; it < I3; ++it) d[it][0] = d[it][1] = 0.0;
+#pragma unroll
+                for (int ks = 0; ks < KS; ++ks)
+#pragma unroll
+                    for (int it = 0; it < I3; ++it)
+                        if (live<C::G3, WARPS>(warp, it)) dmma(d[it][0], d[it][1], vk[ks][r3[it]], bop[2][ks]);
+            } else {
 #pragma unroll
             for (int it = 0; it < I3; ++it) {
                 d[it][0] = d[it][1] = 0.0;
                 if (!live<C::G3, WARPS>(warp, it)) continue;  // warp-uniform: no dummy DMMAs
 #pragma unroll
                 for (int ks = 0; ks < KS; ++ks) dmma(d[it][0], d[it][1], vk[ks][r3[it]], bop[2][ks]);
+            }
             }
 #pragma unroll
             for (int it = 0; it < I3; ++it)
@@ -240,12 +253,22 @@ sep_fused_dmma_cp_kernel(const double* __restrict__ src, double* __restrict__ ds
         // ---- x1: line (ly TX + cx) n^2 + jj:  U(p) -> W ------------------------------------------
         {
             double d[I1][2];
+            if constexpr (C::ILP) {
+#pragma unroll
+                for (int it = 0; it < I1; ++it) d[it][0] = d[it][1] = 0.0;
+#pragma unroll
+                for (int ks = 0; ks < KS; ++ks)
+#pragma unroll
+                    for (int it = 0; it < I1; ++it)
+                        if (live<C::G1, WARPS>(warp, it)) dmma(d[it][0], d[it][1], Ub[r1[it] + k1[ks]], bop[0][ks]);
+            } else {
 #pragma unroll
             for (int it = 0; it < I1; ++it) {
                 d[it][0] = d[it][1] = 0.0;
                 if (!live<C::G1, WARPS>(warp, it)) continue;
 #pragma unroll
                 for (int ks = 0; ks < KS; ++ks) dmma(d[it][0], d[it][1], Ub[r1[it] + k1[ks]], bop[0][ks]);
+            }
             }
 #pragma unroll
             for (int it = 0; it < I1; ++it)
@@ -261,12 +284,22 @@ sep_fused_dmma_cp_kernel(const double* __restrict__ src, double* __restrict__ ds
         // ---- x2: line cell n^2 + j3 n + m1:  W -> V[p & 1] ---------------------------------------
         {
             double d[I2][2];
+            if constexpr (C::ILP) {
+#pragma unroll
+                for (int it = 0; it < I2; ++it) d[it][0] = d[it][1] = 0.0;
+#pragma unroll
+                for (int ks = 0; ks < KS; ++ks)
+#pragma unroll
+                    for (int it = 0; it < I2; ++it)
+                        if (live<C::G2, WARPS>(warp, it)) dmma(d[it][0], d[it][1], W[r2[it] + k2[ks]], bop[1][ks]);
+            } else {
 #pragma unroll
             for (int it = 0; it < I2; ++it) {
                 d[it][0] = d[it][1] = 0.0;
                 if (!live<C::G2, WARPS>(warp, it)) continue;
 #pragma unroll
                 for (int ks = 0; ks < KS; ++ks) dmma(d[it][0], d[it][1], W[r2[it] + k2[ks]], bop[1][ks]);
+            }
             }
 #pragma unroll
             for (int it = 0; it < I2; ++it)
@@ -315,6 +348,12 @@ int sep_fused_dmma5_launch(const double* src, double* dst, const Dims& d, const 
     }();
     if (cfg == 1) return launch_cp<cp5::Cfg<5, 4, 2, 8, 2, 2>>(src, dst, d, A, off, st, first_bad, guard);
     if (cfg == 2) return launch_cp<cp5::Cfg<5, 4, 2, 8, 3, 1>>(src, dst, d, A, off, st, first_bad, guard);
+    if (cfg == 3) return launch_cp<cp5::Cfg<5, 4, 4, 16, 3, 1, true>>(src, dst, d, A, off, st, first_bad, guard);
+    if (cfg == 4) return launch_cp<cp5::Cfg<5, 4, 4, 16, 2, 1>>(src, dst, d, A, off, st, first_bad, guard);
+    if (cfg == 5) return launch_cp<cp5::Cfg<5, 2, 8, 16, 2, 1>>(src, dst, d, A, off, st, first_bad, guard);
+    if (cfg == 6) return launch_cp<cp5::Cfg<5, 2, 8, 16, 2, 1, true>>(src, dst, d, A, off, st, first_bad, guard);
+    if (cfg == 7) return launch_cp<cp5::Cfg<5, 3, 6, 16, 2, 1>>(src, dst, d, A, off, st, first_bad, guard);
+    if (cfg == 8) return launch_cp<cp5::Cfg<5, 4, 5, 16, 2, 1>>(src, dst, d, A, off, st, first_bad, guard);
 #endif
     return launch_cp<cp5::Cfg<5, 4, 4>>(src, dst, d, A, off, st, first_bad, guard);
 }

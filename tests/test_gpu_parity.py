@@ -147,9 +147,11 @@ def test_separable_closer_to_extended_precision_than_reference(order_n):
     assert e_fast <= max(4 * e_ref, 1e-14), (e_fast, e_ref)
 
 
-@pytest.mark.parametrize("order_n", [1, 3, 5])
+@pytest.mark.parametrize("order_n", [1, 2, 3, 4, 5])
 def test_fused_vs_two_pass_separable(order_n):
-    """SPEC acceptance 2 analogue: fused vs two-pass on a random multi-mode IC."""
+    """SPEC acceptance 2 (N=1..3, 12^3, 10 steps, random multi-mode IC, <= 1e-13):
+    bitwise for the literal variant (test_literal_runs_bitwise); for the separable variant the
+    measured gap (r02, tools/mode_gap.py) is the bound's basis, held within ~2x."""
     rng = np.random.default_rng(3)
     terms = tuple(tuple(hb.FourierMode(float(rng.uniform(-1, 1)), int(rng.integers(1, 3)),
                                        float(rng.uniform(0, 6.28))) for _ in range(3)) for _ in range(4))
@@ -165,8 +167,10 @@ def test_fused_vs_two_pass_separable(order_n):
             hb.full_step(st, sc, cfg, ops)
         outs.append(st.data)
     # literal fused vs two-pass is bit-identical (test_literal_runs_bitwise); the separable
-    # two-pass reconstruction carries the reference's cond(H)-amplified rounding
-    tol = {1: 1e-13, 3: 1e-11, 5: 1e-7}[order_n]
+    # two-pass materialises the (2N+2)^3 coefficients and carries their cond(H)-amplified rounding
+    # (SURVEY 8(a) a5), the fused kernel applies the combined operator S H rounded once.
+    # Measured on B200 (r02): 5.2e-15, 5.5e-14, 2.1e-12, 1.8e-10, 2.2e-8 for N = 1..5.
+    tol = {1: 1.2e-14, 2: 1.2e-13, 3: 4.5e-12, 4: 4e-10, 5: 5e-8}[order_n]
     assert rm.rel_err(outs[1], outs[0]) <= tol
 
 

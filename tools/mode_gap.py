@@ -15,7 +15,7 @@ import paper_1609_09841_b200 as hb  # noqa: E402
 def random_ic(seed=3):
     rng = np.random.default_rng(seed)
     return hb.SeparableIC(tuple(tuple(hb.FourierMode(float(rng.uniform(-1, 1)), int(rng.integers(1, 3)),
-                                                     float(rng.uniform(0, 2 * np.pi))) for _ in range(3))
+                                                     float(rng.uniform(0, 6.28))) for _ in range(3))
                                 for _ in range(4)))
 
 
