@@ -475,10 +475,14 @@ static int launch_dm3(const double* src, double* dst, const Dims& d, const SepOp
         const char* e = getenv("H3_DMMA_CLUSTER_Y");
         return e ? atoi(e) : 2;
     }();
+    static const int cx = [] {  // tools library only: H3_DMMA_CLUSTER_X
+        const char* e = getenv("H3_DMMA_CLUSTER_X");
+        return e ? atoi(e) : 1;
+    }();
 #else
-    constexpr int cy = 2;
+    constexpr int cy = 2, cx = 1;
 #endif
-    if (cy > 1 && gy % cy == 0) {
+    if ((cy > 1 || cx > 1) && gy % cy == 0 && gx % cx == 0) {
         cudaLaunchConfig_t lc = {};
         lc.gridDim = dim3((unsigned)gx, (unsigned)gy, (unsigned)gz);
         lc.blockDim = dim3(C::THREADS);
@@ -486,7 +490,7 @@ static int launch_dm3(const double* src, double* dst, const Dims& d, const SepOp
         lc.stream = st;
         cudaLaunchAttribute at[1];
         at[0].id = cudaLaunchAttributeClusterDimension;
-        at[0].val.clusterDim.x = 1;
+        at[0].val.clusterDim.x = cx;
         at[0].val.clusterDim.y = cy;
         at[0].val.clusterDim.z = 1;
         lc.attrs = at;

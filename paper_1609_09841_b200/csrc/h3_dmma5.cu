@@ -42,12 +42,18 @@ using tma::mbar_wait;
 // reads at k-step ks, per pass (x1, x2, x3).  Found by tools/cp5_korder_search.py: a half-warp's
 // 4 lines x 4 k-lanes then fall on distinct bank pairs (x1) or fewer wavefronts (x2),
 // where the natural order k = 4 ks + q is 2-way on every load.  Packed 4 bits per lane q.
+// LAYOUT2 (tools/cp5_smem_model.py, validated against ncu's per-instruction wavefronts): W cell
+// stride n(n^2+1) + 1, V j3 stride n^2 with the second V buffer 8 doubles further, and the x2 order
+// below: modelled wavefronts per plane 2724 -> 2112 (x3 loads 4 -> 2 per instruction).
+template <int LAYOUT2 = 0>
 __device__ __forceinline__ int korder5(int ax, int ks, int q) {
     constexpr unsigned T[3][3] = {{0x7610u, 0x9832u, 0xba54u},   // x1: (q >> 1, 2 ks + (q & 1))
                                   {0xa640u, 0xb751u, 0x9832u},   // x2
                                   {0x3210u, 0x7654u, 0xba98u}};  // x3: natural (the searched
                                   // conflict-free 0x6210 0xa843 0xb975 measured 4 % slower)
-    return (int)((T[ax][ks] >> (4 * q)) & 15u);
+    constexpr unsigned T2[3] = {0x64a0u, 0x1b57u, 0x3892u};      // x2 under LAYOUT2
+    const unsigned t = ((LAYOUT2 & 2) && ax == 1) ? T2[ks] : T[ax][ks];
+    return (int)((t >> (4 * q)) & 15u);
 }
 
 // group `warp + WARPS * it` of a pass with G groups of 8 lines exists (warp-uniform; constant
@@ -57,8 +63,11 @@ __device__ __forceinline__ bool live(int warp, int it) {
     return G % WARPS == 0 || warp + WARPS * it < G;
 }
 
-template <int N_, int TX_, int TY_, int WARPS_ = 16, int STAGES_ = 3, int MINB_ = 1, bool ILP_ = false>
+template <int N_, int TX_, int TY_, int WARPS_ = 16, int STAGES_ = 3, int MINB_ = 1, bool ILP_ = false,
+          int LAYOUT2_ = 0>
 struct Cfg {
+    // LAYOUT2 bit 0: the V layout (x3 loads); bit 1: the W layout + x2 K order (x2 loads)
+    static constexpr int LAYOUT2 = LAYOUT2_;
     // ILP: issue a pass's DMMAs k-step-major (all line groups of the warp at k-step 0, then 1, 2),
     // so consecutive DMMAs are independent, instead of one group's 3-deep accumulation chain
     static constexpr bool ILP = ILP_;
@@ -69,14 +78,14 @@ struct Cfg {
     static constexpr int TX = TX_, TY = TY_, NX = TX + 1, NY = TY + 1, NNODE = NX * NY;
     static constexpr int WARPS = WARPS_, THREADS = 32 * WARPS, STAGES = STAGES_, MINB = MINB_;
     static constexpr int UNS = n3;                   // U: dense node blocks [j3][j2][j1]
-    static constexpr int WM = n2 + 1, WCS = n * WM;  // W: [node row][cell][m1][j3 j2], odd m1 stride
-    static constexpr int VJ = n2 + 1, VCS = n * VJ;  // V: [cell][j3][m2 m1]
+    static constexpr int WM = n2 + 1, WCS = n * WM + ((LAYOUT2 & 2) ? 1 : 0);  // W: [node row][cell][m1][j3 j2]
+    static constexpr int VJ = (LAYOUT2 & 1) ? n2 : n2 + 1, VCS = n * VJ;       // V: [cell][j3][m2 m1]
     static constexpr int G1 = (NY * TX * n2 + 7) / 8;  // x1 line groups of 8
     static constexpr int G2 = (TY * TX * n2 + 7) / 8;  // x2 line groups
     static constexpr int G3 = (TY * TX * n2 + 7) / 8;  // x3 line groups
     static constexpr size_t U_D = (size_t)NNODE * UNS;
     static constexpr size_t W_D = (size_t)NY * TX * WCS;
-    static constexpr size_t V_D = (size_t)TY * TX * VCS;
+    static constexpr size_t V_D = (size_t)TY * TX * VCS + ((LAYOUT2 & 1) ? 8 : 0);  // one V buffer (+ bank shift)
     static constexpr size_t SMEM_DATA = (STAGES * U_D + W_D + 2 * V_D) * sizeof(double);
     static constexpr size_t SMEM = SMEM_DATA + STAGES * sizeof(uint64_t);
     static_assert(NY <= WARPS, "one loader warp per tile row");
@@ -119,7 +128,7 @@ sep_fused_dmma_cp_kernel(const double* __restrict__ src, double* __restrict__ ds
             // x1 orders its K inputs as (vertex q >> 1, component 2 ks + (q & 1)) instead of
             // k = 4 ks + q: with the 6-double line rows of a node block this puts the 16 lanes of a
             // half-warp on 16 distinct bank pairs (found by search; the natural order is 2-way)
-            const int kc = C::N == 5 ? korder5(ax, ks, q) : 4 * ks + q;
+            const int kc = C::N == 5 ? korder5<C::LAYOUT2>(ax, ks, q) : 4 * ks + q;
             bop[ax][ks] = g < n ? p.A[ax][g < n ? g : 0][kc] : 0.0;
         }
 
@@ -171,9 +180,9 @@ sep_fused_dmma_cp_kernel(const double* __restrict__ src, double* __restrict__ ds
 #pragma unroll
     for (int ks = 0; ks < KS; ++ks) {
         // per pass, the (vertex a, component j) this lane's k-slot reads (korder5: N = 5)
-        const int c1 = C::N == 5 ? korder5(0, ks, q) : 4 * ks + q;
-        const int c2 = C::N == 5 ? korder5(1, ks, q) : 4 * ks + q;
-        const int c3 = C::N == 5 ? korder5(2, ks, q) : 4 * ks + q;
+        const int c1 = C::N == 5 ? korder5<C::LAYOUT2>(0, ks, q) : 4 * ks + q;
+        const int c2 = C::N == 5 ? korder5<C::LAYOUT2>(1, ks, q) : 4 * ks + q;
+        const int c3 = C::N == 5 ? korder5<C::LAYOUT2>(2, ks, q) : 4 * ks + q;
         k1[ks] = (c1 / n) * UNS + c1 % n;       // x1: node cx + a along the row
         k2[ks] = (c2 / n) * TX * WCS + c2 % n;  // x2: cell row cy + a
         ka[ks] = c3 / n;                        // x3: plane p - 1 + a ...
@@ -354,6 +363,10 @@ int sep_fused_dmma5_launch(const double* src, double* dst, const Dims& d, const 
     if (cfg == 6) return launch_cp<cp5::Cfg<5, 2, 8, 16, 2, 1, true>>(src, dst, d, A, off, st, first_bad, guard);
     if (cfg == 7) return launch_cp<cp5::Cfg<5, 3, 6, 16, 2, 1>>(src, dst, d, A, off, st, first_bad, guard);
     if (cfg == 8) return launch_cp<cp5::Cfg<5, 4, 5, 16, 2, 1>>(src, dst, d, A, off, st, first_bad, guard);
+    if (cfg == 9) return launch_cp<cp5::Cfg<5, 4, 4, 16, 3, 1, false, 3>>(src, dst, d, A, off, st, first_bad, guard);
+    if (cfg == 10) return launch_cp<cp5::Cfg<5, 4, 4, 16, 2, 1, false, 3>>(src, dst, d, A, off, st, first_bad, guard);
+    if (cfg == 11) return launch_cp<cp5::Cfg<5, 4, 4, 16, 3, 1, false, 1>>(src, dst, d, A, off, st, first_bad, guard);
+    if (cfg == 12) return launch_cp<cp5::Cfg<5, 4, 4, 16, 3, 1, false, 2>>(src, dst, d, A, off, st, first_bad, guard);
 #endif
     return launch_cp<cp5::Cfg<5, 4, 4>>(src, dst, d, A, off, st, first_bad, guard);
 }
