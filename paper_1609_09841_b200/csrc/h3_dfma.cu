@@ -269,9 +269,13 @@ int recon_sep_launch(const double* src, double* coeff, const Dims& d, int order_
         case 0: return recon_sep_n<0>(src, coeff, d, h_mat, off, st, guard);
         case 1: return recon_sep_n<1>(src, coeff, d, h_mat, off, st, guard);
         case 2: return recon_sep_n<2>(src, coeff, d, h_mat, off, st, guard);
-        case 3: return recon_sep_n<3>(src, coeff, d, h_mat, off, st, guard);
         case 4: return recon_sep_n<4>(src, coeff, d, h_mat, off, st, guard);
+#ifdef H3_MEASURE
+        // N = 3, 5 reconstruct on the FP64 tensor cores (h3_dmma.cu, h3_dmma5.cu); the DFMA
+        // kernels for them are A/B references of the tools library (H3_RECON_IMPL=sep)
+        case 3: return recon_sep_n<3>(src, coeff, d, h_mat, off, st, guard);
         case 5: return recon_sep_n<5>(src, coeff, d, h_mat, off, st, guard);
+#endif
     }
     return (int)cudaErrorInvalidValue;
 }

@@ -355,6 +355,7 @@ int sep_fused_dmma5_launch(const double* src, double* dst, const Dims& d, const 
         const char* e = getenv("H3_DMMA5_CFG");
         return e ? atoi(e) : 0;
     }();
+    if (cfg >= 20) return sep_fused_dmma5_ws_launch(src, dst, d, A, off, st, first_bad, guard, cfg - 20);
     if (cfg == 1) return launch_cp<cp5::Cfg<5, 4, 2, 8, 2, 2>>(src, dst, d, A, off, st, first_bad, guard);
     if (cfg == 2) return launch_cp<cp5::Cfg<5, 4, 2, 8, 3, 1>>(src, dst, d, A, off, st, first_bad, guard);
     if (cfg == 3) return launch_cp<cp5::Cfg<5, 4, 4, 16, 3, 1, true>>(src, dst, d, A, off, st, first_bad, guard);
@@ -367,8 +368,10 @@ int sep_fused_dmma5_launch(const double* src, double* dst, const Dims& d, const 
     if (cfg == 10) return launch_cp<cp5::Cfg<5, 4, 4, 16, 2, 1, false, 3>>(src, dst, d, A, off, st, first_bad, guard);
     if (cfg == 11) return launch_cp<cp5::Cfg<5, 4, 4, 16, 3, 1, false, 1>>(src, dst, d, A, off, st, first_bad, guard);
     if (cfg == 12) return launch_cp<cp5::Cfg<5, 4, 4, 16, 3, 1, false, 2>>(src, dst, d, A, off, st, first_bad, guard);
+    if (cfg == 13) return launch_cp<cp5::Cfg<5, 4, 4>>(src, dst, d, A, off, st, first_bad, guard);  // r01 default
 #endif
-    return launch_cp<cp5::Cfg<5, 4, 4>>(src, dst, d, A, off, st, first_bad, guard);
+    // the warp-specialised pipeline (h3_dmma5ws.cu) replaces this lock-step march (r02: +15 %)
+    return sep_fused_dmma5_ws_launch(src, dst, d, A, off, st, first_bad, guard, 0);
 }
 
 // ---------------------------------------------------------------------------------------------

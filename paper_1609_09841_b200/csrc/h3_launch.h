@@ -72,6 +72,9 @@ int sep_fused_dmma3_launch(const double* src, double* dst, const Dims& d, const 
 int sep_fused_dmma5_launch(const double* src, double* dst, const Dims& d, const double* A, int off,
                            cudaStream_t st, unsigned long long* first_bad,
                            const unsigned long long* guard);
+int sep_fused_dmma5_ws_launch(const double* src, double* dst, const Dims& d, const double* A, int off,
+                              cudaStream_t st, unsigned long long* first_bad, const unsigned long long* guard,
+                              int variant);
 int recon_dmma5_launch(const double* src, double* coeff, const Dims& d, const double* h_mat, int off,
                        cudaStream_t st, const unsigned long long* guard);
 int recon_dmma3_launch(const double* src, double* coeff, const Dims& d, const double* h_mat, int off,

@@ -231,8 +231,13 @@ static int dispatch_mode(int mode, bool fast, const T* in, T* out, const Dims& d
         case 0:
             return launch_one<T, N, 0, false>(in, out, d, ops, off, st, first_bad, guard);
         case 1:
-            return fast ? launch_one<T, N, 1, true>(in, out, d, ops, off, st, first_bad, guard)
-                        : launch_one<T, N, 1, false>(in, out, d, ops, off, st, first_bad, guard);
+#ifdef H3_MEASURE
+            // the FMA per-cell sweeps (H3_RECON_IMPL=fma) exist in the tools library only
+            if (fast) return launch_one<T, N, 1, true>(in, out, d, ops, off, st, first_bad, guard);
+#else
+            (void)fast;
+#endif
+            return launch_one<T, N, 1, false>(in, out, d, ops, off, st, first_bad, guard);
         case 2:
             return launch_one<T, N, 2, false>(in, out, d, ops, off, st, first_bad, guard);
     }
