@@ -148,17 +148,19 @@ sep_fused_dmma_ws_kernel(const double* __restrict__ src, double* __restrict__ ds
     const int64_t plane_elems = (int64_t)M1 * M2 * n3;
 
     if (tid == 0) {
+        // consumer hand-offs count every thread of the releasing role: each lane's own arrive (one
+        // warp-wide instruction) releases its own shared-memory writes / reads
         for (int s = 0; s < SU; ++s) {
             mbar_init(&u_full[s], 1);
-            mbar_init(&u_empty[s], C::N1);
+            mbar_init(&u_empty[s], 32 * C::N1);
         }
         for (int b = 0; b < C::NWB; ++b) {
-            mbar_init(&w_full[b], C::N1);
-            mbar_init(&w_empty[b], C::N2);
+            mbar_init(&w_full[b], 32 * C::N1);
+            mbar_init(&w_empty[b], 32 * C::N2);
         }
         for (int b = 0; b < C::NVB; ++b) {
-            mbar_init(&v_full[b], C::N2);
-            mbar_init(&v_empty[b], C::N3);
+            mbar_init(&v_full[b], 32 * C::N2);
+            mbar_init(&v_empty[b], 32 * C::N3);
         }
         mbar_fence_init();
     }
@@ -247,11 +249,8 @@ sep_fused_dmma_ws_kernel(const double* __restrict__ src, double* __restrict__ ds
                     }
                 }
             }
-            __syncwarp();
-            if (lane == 0) {
-                mbar_arrive(&u_empty[s]);
-                mbar_arrive(&w_full[b]);
-            }
+            mbar_arrive(&u_empty[s]);
+            mbar_arrive(&w_full[b]);
         }
     } else if (warp <= C::N1 + C::N2) {
         // ---- x2: line cell n^2 + j3 n + m1 : W[t & 1] -> V[t % 3] ----------------------------------
@@ -299,11 +298,8 @@ sep_fused_dmma_ws_kernel(const double* __restrict__ src, double* __restrict__ ds
                     }
                 }
             }
-            __syncwarp();
-            if (lane == 0) {
-                mbar_arrive(&w_empty[b]);
-                mbar_arrive(&v_full[v]);
-            }
+            mbar_arrive(&w_empty[b]);
+            mbar_arrive(&v_full[v]);
         }
     } else {
         // ---- x3: line cell n^2 + (m2 n + m1) : V(c), V(c+1) -> dst cell plane c --------------------
@@ -348,10 +344,7 @@ sep_fused_dmma_ws_kernel(const double* __restrict__ src, double* __restrict__ ds
 #pragma unroll
                     for (int ks = 0; ks < KS; ++ks) dmma(acc[j][0], acc[j][1], vk[ks][rd[it]], bop[ks]);
                 }
-                if (i0 + C::B3 >= I) {  // the last batch has read V(c): release it before the stores
-                    __syncwarp();
-                    if (lane == 0) mbar_arrive(&v_empty[v0]);  // V(c+1) is released at c+1
-                }
+                if (i0 + C::B3 >= I) mbar_arrive(&v_empty[v0]);  // V(c) read: release it (V(c+1) at c+1)
 #pragma unroll
                 for (int j = 0; j < C::B3; ++j) {
                     const int it = i0 + j;

@@ -1,6 +1,7 @@
 cd "$GRAFT_REPO_ROOT" 2>/dev/null || cd /root/repo
 mkdir -p gpurun_out
-timeout 2400 python -m pytest tests -m gpu -q -x --durations=15 > gpurun_out/r2l_pytest_gpu.log 2>&1; echo "rc=$?" >> gpurun_out/r2l_pytest_gpu.log
-for tool in memcheck racecheck synccheck; do timeout 900 compute-sanitizer --tool $tool --kernel-name regex:dmma_ws python tools/sanitize.py > gpurun_out/r2l_san_$tool.txt 2>&1; echo "rc=$?" >> gpurun_out/r2l_san_$tool.txt; done
-timeout 900 python bench.py --no-cpu > gpurun_out/r2l_bench.json 2> gpurun_out/r2l_bench.err; echo "rc=$?" >> gpurun_out/r2l_bench.err
+timeout 900 compute-sanitizer --tool racecheck --racecheck-report all python tools/sanitize_ws.py > gpurun_out/r2o_race.txt 2>&1
+timeout 900 compute-sanitizer --tool synccheck python tools/sanitize_ws.py 17 9 31 > gpurun_out/r2o_sync.txt 2>&1
+for c in 45; do H3_LIB=build/libh3b200_measure.so H3_DMMA5_CFG=$c timeout 90 python tools/variant_check.py 5 40 36 20; done > gpurun_out/r2o_check.txt 2>&1
+tools/ab.sh 3 "ws:" "lockstep:H3_DMMA5_CFG=13" -- tools/time_fused.py 5 256 fused 4 > gpurun_out/r2o_ab5.txt 2>&1
 echo done
