@@ -523,6 +523,8 @@ int sep_fused_dmma3_launch(const double* src, double* dst, const Dims& d, const 
         const char* e = getenv("H3_DMMA_CFG");
         return e ? atoi(e) : 0;
     }();
+    if (cfg >= 200) return sep_fused_dmma3x_launch(src, dst, d, ops, off, st, first_bad, guard, cfg - 200);
+    if (cfg >= 100) return sep_fused_dmma3_ws_launch(src, dst, d, ops, off, st, first_bad, guard, cfg - 100);
     switch (cfg) {
         case 6: return launch_dm3<Dm3Cfg<7, 16, 3, true>>(src, dst, d, ops, off, st, first_bad, guard);  // cp.async loads
         case 11: return launch_dm3<Dm3Cfg<7, 16, 3, true, 1, 1, true>>(src, dst, d, ops, off, st, first_bad, guard);

@@ -69,6 +69,12 @@ int sep_fused_launch(const double* src, double* dst, const Dims& d, int order_n,
 int sep_fused_dmma3_launch(const double* src, double* dst, const Dims& d, const double* A, int off,
                            cudaStream_t st, unsigned long long* first_bad,
                            const unsigned long long* guard);
+int sep_fused_dmma3_ws_launch(const double* src, double* dst, const Dims& d, const SepOps<3>& ops, int off,
+                              cudaStream_t st, unsigned long long* first_bad, const unsigned long long* guard,
+                              int variant);
+int sep_fused_dmma3x_launch(const double* src, double* dst, const Dims& d, const SepOps<3>& ops, int off,
+                            cudaStream_t st, unsigned long long* first_bad, const unsigned long long* guard,
+                            int variant);
 int sep_fused_dmma5_launch(const double* src, double* dst, const Dims& d, const double* A, int off,
                            cudaStream_t st, unsigned long long* first_bad,
                            const unsigned long long* guard);
