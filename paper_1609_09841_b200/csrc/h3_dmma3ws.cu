@@ -20,6 +20,9 @@
 // k & 1); a producer's first wait on an "empty" barrier passes at once (parity 1 of a fresh
 // barrier).  Every lane of a releasing role arrives (counts 32 x warps), so each lane's own
 // shared-memory accesses are ordered by its own release.
+// Measurement-only (tools build, -DH3_MEASURE): measured slower than the lock-step kernel, see
+// profiles/r02_m3_ws_variants.txt; the product library does not contain it.
+#ifdef H3_MEASURE
 #include "h3_launch.h"
 #include "h3_tma.cuh"
 
@@ -413,3 +416,4 @@ int sep_fused_dmma3_ws_launch(const double* src, double* dst, const Dims& d, con
 }
 
 }  // namespace h3
+#endif  // H3_MEASURE

@@ -28,6 +28,9 @@
 // V[(p - 1) & 1].  Input planes arrive by TMA bulk row copies into a 3-stage mbarrier ring; the
 // tile rows are padded to 584 doubles so the two node rows of an x1 fragment hit disjoint bank
 // halves.
+// Measurement-only (tools build, -DH3_MEASURE): measured slower than the lock-step kernel, see
+// profiles/r02_m3_ws_variants.txt; the product library does not contain it.
+#ifdef H3_MEASURE
 #include "h3_launch.h"
 #include "h3_tma.cuh"
 
@@ -250,40 +253,38 @@ sep_fused_dmma3x_kernel(const double* __restrict__ src, double* __restrict__ dst
             if (pl == 0) continue;
             const int t = pl - 1;  // node plane whose V this iteration contracts
             const double* Vb = V + (t & 1) * C::V_D + vbase;
-            double* oplane = dst + (zc0 + t - 1) * plane_elems;
-            double* ob = oplane + obase;
-            asm volatile("" : "+l"(ob));  // one 64-bit base per plane, per-chain offsets added to it
+            double* ob = dst + (zc0 + t - 1) * plane_elems + obase;
+            // chain k completes cell plane t-1 in the lanes with par == (t + k + 1) & 1
+            const bool de = par == ((t + 1) & 1);  // even chains
             unsigned screen = 0x7ff00000u;
+            double a[K3];
 #pragma unroll
-            for (int k0 = 0; k0 < K3; k0 += C::B3) {
-                constexpr int B = C::B3;
-                double a[B];
+            for (int k = 0; k < K3; ++k) a[k] = Vb[va(k)];
 #pragma unroll
-                for (int b = 0; b < B; ++b)
-                    if (k0 + b < K3) a[b] = Vb[va(k0 + b)];
-#pragma unroll
-                for (int b = 0; b < B; ++b) {
-                    const int k = k0 + b;
-                    if (k >= K3) continue;
-                    dmma(acc[k][0], acc[k][1], a[b], ((t + k) & 1) ? b1 : b0);
-                    const bool done = par == ((t + k + 1) & 1);
-                    if (t > 0) {
-                        if (done && (live >> k & 1u)) {
-                            double* o = ob + (cyk(k) * rowstep + cxk(k) * n3);
-                            __stcs(o, acc[k][0]);
-                            __stcs(o + 16, acc[k][1]);
-                        }
-                        screen = min(screen, min(exp_gap(acc[k][0]), exp_gap(acc[k][1])));
-                    }
-                    acc[k][0] = done ? 0.0 : acc[k][0];
-                    acc[k][1] = done ? 0.0 : acc[k][1];
+            for (int k = 0; k < K3; ++k) {
+                const bool done = (k & 1) ? !de : de;
+                dmma(acc[k][0], acc[k][1], a[k], ((t + k) & 1) ? b1 : b0);
+                if (t > 0) {
+                    // predicated streaming stores (no branch): finished lanes of live chains
+                    double* o = ob + (cyk(k) * rowstep + cxk(k) * n3);
+                    const unsigned pr = (unsigned)(done && (live >> k & 1u));
+                    asm volatile(
+                        "{\n.reg .pred p;\nsetp.ne.u32 p, %3, 0;\n"
+                        "@p st.global.cs.f64 [%0], %1;\n@p st.global.cs.f64 [%0+128], %2;\n}\n" ::"l"(o),
+                        "d"(acc[k][0]), "d"(acc[k][1]), "r"(pr)
+                        : "memory");
+                    screen = min(screen, min(exp_gap(acc[k][0]), exp_gap(acc[k][1])));
                 }
+                acc[k][0] = done ? 0.0 : acc[k][0];
+                acc[k][1] = done ? 0.0 : acc[k][1];
             }
             if (t > 0 && screen == 0u) {  // rare: some lane holds Inf/NaN -- locate it exactly
+                double* oplane = dst + (zc0 + t - 1) * plane_elems;
 #pragma unroll
                 for (int k = 0; k < K3; ++k) {
-                    const bool done = par == ((t + k + 1) & 1);
-                    if (done && (live >> k & 1u) && (!isfinite(oplane[ooff(k)]) || !isfinite(oplane[ooff(k) + 16])))
+                    const bool done = (k & 1) ? !de : de;
+                    if (done && (live >> k & 1u) &&
+                        (!isfinite(oplane[ooff(k)]) || !isfinite(oplane[ooff(k) + 16])))
                         flag_bad(first_bad, (zc0 + t - 1) * M2 * (int64_t)M1 + ooff(k) / n3);
                 }
             }
@@ -342,3 +343,4 @@ int sep_fused_dmma3x_launch(const double* src, double* dst, const Dims& d, const
 }
 
 }  // namespace h3
+#endif  // H3_MEASURE
