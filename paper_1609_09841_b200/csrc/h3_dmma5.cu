@@ -600,6 +600,14 @@ recon_dmma_cp_kernel(const double* __restrict__ src, double* __restrict__ coeff,
 
 int recon_dmma5_launch(const double* src, double* coeff, const Dims& d, const double* h_mat, int off,
                        cudaStream_t st, const unsigned long long* guard) {
+    // the warp-specialised pipeline (h3_recon5ws.cu) is the product kernel; the lock-step kernel
+    // below stays in the tools library as its A/B baseline (H3_RECON5_WS=-1)
+#ifdef H3_MEASURE
+    static const int ws = [] {  // tools library only: H3_RECON5_WS=k selects a variant
+        const char* e = getenv("H3_RECON5_WS");
+        return e ? atoi(e) : 0;
+    }();
+    if (ws >= 0) return recon_dmma5_ws_launch(src, coeff, d, h_mat, off, st, guard, ws);
     using C = rcp::Cfg<5, 4, 2, 2>;
     const int64_t nz = d.z_end - d.z_begin;
     if (nz <= 0) return 0;
@@ -619,6 +627,9 @@ int recon_dmma5_launch(const double* src, double* coeff, const Dims& d, const do
     kern<<<dim3((unsigned)gx, (unsigned)gy, (unsigned)gz), C::THREADS, C::SMEM, st>>>(src, coeff, d, off, (int)zchunk,
                                                                                    hp, guard);
     return (int)cudaGetLastError();
+#else
+    return recon_dmma5_ws_launch(src, coeff, d, h_mat, off, st, guard, 0);
+#endif
 }
 
 }  // namespace h3

@@ -83,6 +83,8 @@ int sep_fused_dmma5_ws_launch(const double* src, double* dst, const Dims& d, con
                               int variant);
 int recon_dmma5_launch(const double* src, double* coeff, const Dims& d, const double* h_mat, int off,
                        cudaStream_t st, const unsigned long long* guard);
+int recon_dmma5_ws_launch(const double* src, double* coeff, const Dims& d, const double* h_mat, int off,
+                          cudaStream_t st, const unsigned long long* guard, int variant);
 int recon_dmma3_launch(const double* src, double* coeff, const Dims& d, const double* h_mat, int off,
                        cudaStream_t st, const unsigned long long* guard);
 int recon_sep_launch(const double* src, double* coeff, const Dims& d, int order_n, const double* h_mat,

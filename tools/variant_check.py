@@ -2,7 +2,7 @@
 of each parity on a smooth random field, separable (the variant selected by the H3_* knobs) vs
 the literal kernel of the same library (the reference's arithmetic).
 
-usage: H3_LIB=build/libh3b200_measure.so H3_DMMA5_CFG=9 python tools/variant_check.py 5 40 36 20
+usage: H3_LIB=build/libh3b200_measure.so H3_DMMA5_CFG=9 python tools/variant_check.py 5 40 36 20 [MODE]
 """
 import os
 import sys
@@ -17,6 +17,7 @@ import paper_1609_09841_b200 as hb  # noqa: E402
 
 n = int(sys.argv[1])
 cells = tuple(int(v) for v in sys.argv[2:5])
+mode = sys.argv[5] if len(sys.argv) > 5 else "fused"
 grid = hb.GridSpec(cells)
 rng = np.random.default_rng(5)
 ic = hb.SeparableIC(tuple(tuple(hb.FourierMode(float(rng.uniform(-1, 1)), int(rng.integers(1, 4)),
@@ -30,11 +31,11 @@ for parity in ("primary", "dual"):
     outs = {}
     for variant in ("literal", "separable"):
         dst = hb.DofField.zeros(other, n)
-        hb.half_step(src, dst, hb.StepConfig(variant=variant), hb.OperatorSet.for_grid(grid, n))
+        hb.half_step(src, dst, hb.StepConfig(variant=variant, mode=mode), hb.OperatorSet.for_grid(grid, n))
         outs[variant] = dst.tensor
     err = float((outs["separable"] - outs["literal"]).abs().max() / outs["literal"].abs().max())
     worst = max(worst, err)
 env = " ".join(f"{k}={v}" for k, v in os.environ.items() if k.startswith("H3_") and k != "H3_LIB")
-print(f"variant_check N={n} cells={cells} [{env}] separable vs literal (one half step, both parities): "
+print(f"variant_check N={n} cells={cells} {mode} [{env}] separable vs literal (one half step, both parities): "
       f"{worst:.3e} {'OK' if worst <= (5e-9 if n >= 5 else 1e-12) else 'FAIL'}", flush=True)
 torch.cuda.synchronize()
