@@ -113,7 +113,7 @@ __device__ __forceinline__ unsigned exp_gap(double x) {
 template <class C>
 __global__ void __launch_bounds__(C::THREADS, C::MINB)
 sep_fused_dmma3_kernel(const double* __restrict__ src, double* __restrict__ dst, Dims d, int off,
-                       int zchunk, const __grid_constant__ SepOps<3> p,
+                       int zchunk, int band, int cy, const __grid_constant__ SepOps<3> p,
                        unsigned long long* first_bad, const unsigned long long* guard) {
     constexpr int n = C::n, n3 = C::n3, TX = C::TX, TY = C::TY, NX = C::NX, NY = C::NY;
     constexpr int NCOL = C::NCOL, WARPS = C::WARPS, STAGES = C::STAGES, UNS = C::UNS;
@@ -128,7 +128,9 @@ sep_fused_dmma3_kernel(const double* __restrict__ src, double* __restrict__ dst,
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int q = lane & 3, g = lane >> 2, par = q >> 1;  // fragment coordinates
     const int M1 = (int)d.M1, M2 = (int)d.M2;
-    const int cx0 = blockIdx.x * TX, cy0 = blockIdx.y * TY;
+    int tbx, tby;
+    band_tile(band, cy, tbx, tby);
+    const int cx0 = tbx * TX, cy0 = tby * TY;
     const int64_t zc0 = d.z_begin + (int64_t)blockIdx.z * zchunk;
     const int64_t zc1 = min(zc0 + (int64_t)zchunk, d.z_end);
     const int P = (int)(zc1 - zc0) + 1;
@@ -453,6 +455,11 @@ sep_fused_dmma3_kernel(const double* __restrict__ src, double* __restrict__ dst,
     cp_async_wait<0>();
 }
 
+// column-band width of the tile rasterisation (band_tile, h3_launch.h)
+#ifndef H3_DMMA3_BAND
+#define H3_DMMA3_BAND 0
+#endif
+
 template <class C>
 static int launch_dm3(const double* src, double* dst, const Dims& d, const SepOps<3>& ops, int off,
                       cudaStream_t st, unsigned long long* first_bad,
@@ -479,10 +486,17 @@ static int launch_dm3(const double* src, double* dst, const Dims& d, const SepOp
         const char* e = getenv("H3_DMMA_CLUSTER_X");
         return e ? atoi(e) : 1;
     }();
+    static const int band = [] {  // tools library only: H3_DMMA_BAND (0 = plain row order)
+        const char* e = getenv("H3_DMMA_BAND");
+        return e ? atoi(e) : H3_DMMA3_BAND;
+    }();
 #else
-    constexpr int cy = 2, cx = 1;
+    constexpr int cy = 2, cx = 1, band = H3_DMMA3_BAND;
 #endif
-    if ((cy > 1 || cx > 1) && gy % cy == 0 && gx % cx == 0) {
+    const bool clustered = (cy > 1 || cx > 1) && gy % cy == 0 && gx % cx == 0;
+    const int cy_eff = clustered ? cy : 1;
+    const int band_eff = cx > 1 ? 0 : band;  // the band map keeps y clusters only
+    if (clustered) {
         cudaLaunchConfig_t lc = {};
         lc.gridDim = dim3((unsigned)gx, (unsigned)gy, (unsigned)gz);
         lc.blockDim = dim3(C::THREADS);
@@ -495,11 +509,11 @@ static int launch_dm3(const double* src, double* dst, const Dims& d, const SepOp
         at[0].val.clusterDim.z = 1;
         lc.attrs = at;
         lc.numAttrs = 1;
-        e = cudaLaunchKernelEx(&lc, kern, src, dst, d, off, (int)zchunk, ops, first_bad, guard);
+        e = cudaLaunchKernelEx(&lc, kern, src, dst, d, off, (int)zchunk, band_eff, cy_eff, ops, first_bad, guard);
         return (int)e;
     }
     kern<<<dim3((unsigned)gx, (unsigned)gy, (unsigned)gz), C::THREADS, C::SMEM, st>>>(
-        src, dst, d, off, (int)zchunk, ops, first_bad, guard);
+        src, dst, d, off, (int)zchunk, band_eff, cy_eff, ops, first_bad, guard);
     return (int)cudaGetLastError();
 }
 

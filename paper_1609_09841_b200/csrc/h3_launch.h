@@ -104,6 +104,26 @@ int check_finite_launch(const double* field, int64_t M1, int64_t M2, int64_t M3,
 
 int num_sms();
 
+// Tile rasterisation.  The hardware starts CTAs in linear block order (x fastest), so with a plain
+// mapping the CTAs resident at one time cover ~148 / gx full tile rows: every tile on the lower
+// edge of that strip re-reads its halo node row from DRAM when the next strip runs (the row was
+// evicted long before).  `band_tile` walks the tile grid in column bands of `band` tiles instead
+// (row-major inside a band), so the resident CTAs cover a compact block whose perimeter -- the
+// only halo that misses L2 -- is ~3x shorter.  Clusters of `cy` CTAs along y keep their pairing:
+// the unit remapped is the cluster (x, y / cy); band = 0 is the identity.
+__device__ __forceinline__ void band_tile(int band, int cy, int& bx, int& by) {
+    bx = (int)blockIdx.x;
+    by = (int)blockIdx.y;
+    if (band <= 0) return;
+    const int gx = (int)gridDim.x, gu = (int)gridDim.y / cy;
+    const int lin = bx + gx * (by / cy);
+    const int b = lin / (band * gu), r = lin - b * (band * gu);
+    const int w = min(band, gx - b * band);  // width of this band (the last one may be narrower)
+    const int uy = r / w;
+    bx = b * band + (r - uy * w);
+    by = uy * cy + (int)blockIdx.y % cy;
+}
+
 // z-chunk length for a tile march over nz cell planes with `tiles` x1-x2 tiles and `slots`
 // resident CTAs: minimises waves x (planes per CTA + halo plane + ~2 planes of pipeline fill),
 // waves = ceil(tiles * chunks / slots), over chunk lengths >= min_chunk.  (At 512^3 m=3 this is

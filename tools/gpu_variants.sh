@@ -4,6 +4,7 @@
 #   interleaved timing vs the product library (tools/ab.sh), optional ncu --set full capture.
 #
 # usage: tools/gpu_variants.sh FAMILY TAG "VARIANTS" [PROFILE_VARIANT]
+#   a variant is a number k (sets the family's variable to k) or any H3_* assignment (H3_DMMA_BAND=8)
 #   FAMILY m3: m=3 fused kernels        (H3_DMMA_CFG:  10x warp-specialised, 20x x1->x2 chained)
 #          m5: m=5 fused kernels        (H3_DMMA5_CFG: lock-step shapes, 20+k warp-specialised)
 #          r5: m=5 reconstruction       (H3_RECON5_WS: warp-specialised variants)
@@ -18,17 +19,18 @@ case $family in
 esac
 mkdir -p gpurun_out
 make -C paper_1609_09841_b200/csrc measure -j16 > gpurun_out/${tag}_make.txt 2>&1
+setting() { if [[ $1 == *=* ]]; then echo "$1"; else echo "$var=$1"; fi; }
 for c in $variants; do
   for shape in "40 36 20" "16 14 9" "9 7 5"; do
-    env H3_LIB=build/libh3b200_measure.so $var=$c timeout 120 python tools/variant_check.py $order $shape $mode
+    env H3_LIB=build/libh3b200_measure.so $(setting $c) timeout 120 python tools/variant_check.py $order $shape $mode
   done
 done > gpurun_out/${tag}_check.txt 2>&1
 args=("base:")
-for c in $variants; do args+=("v$c:$var=$c"); done
+for c in $variants; do args+=("v$c:$(setting $c)"); done
 tools/ab.sh 2 "${args[@]}" -- tools/time_fused.py $order $tsize $mode $tsteps > gpurun_out/${tag}_ab.txt 2>&1
 if [ -n "$prof" ]; then
-  env H3_LIB=build/libh3b200_measure.so $var=$prof timeout 600 ncu --set full --clock-control none --import-source on \
-    -k regex:$kre -s 2 -c 1 -o gpurun_out/${tag}_v$prof -f python tools/time_fused.py $order $psize $mode 1 \
+  env H3_LIB=build/libh3b200_measure.so $(setting $prof) timeout 600 ncu --set full --clock-control none --import-source on \
+    -k regex:$kre -s 2 -c 1 -o gpurun_out/${tag}_v${prof//=/_} -f python tools/time_fused.py $order $psize $mode 1 \
     > gpurun_out/${tag}_prof.txt 2>&1
 fi
 echo done
