@@ -455,9 +455,12 @@ sep_fused_dmma3_kernel(const double* __restrict__ src, double* __restrict__ dst,
     cp_async_wait<0>();
 }
 
-// column-band width of the tile rasterisation (band_tile, h3_launch.h)
+// column-band widths of the tile rasterisation (band_tile, h3_launch.h)
 #ifndef H3_DMMA3_BAND
-#define H3_DMMA3_BAND 0
+#define H3_DMMA3_BAND 8
+#endif
+#ifndef H3_RC3_BAND
+#define H3_RC3_BAND 0
 #endif
 
 template <class C>
@@ -600,7 +603,9 @@ recon_dmma3_kernel(const double* __restrict__ src, double* __restrict__ coeff, D
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int q = lane & 3, g = lane >> 2;
     const int M1 = (int)d.M1, M2 = (int)d.M2;
-    const int cx0 = blockIdx.x * TX, cy0 = blockIdx.y * TY;
+    int tbx, tby;
+    band_tile(d.band, 1, tbx, tby);
+    const int cx0 = tbx * TX, cy0 = tby * TY;
     const int64_t zc0 = d.z_begin + (int64_t)blockIdx.z * zchunk;
     const int64_t zc1 = min(zc0 + (int64_t)zchunk, d.z_end);
     const int P = (int)(zc1 - zc0) + 1;
@@ -763,8 +768,10 @@ int recon_dmma3_launch(const double* src, double* coeff, const Dims& d, const do
     const int64_t gx = (d.M1 + TX - 1) / TX, gy = (d.M2 + TY - 1) / TY;
     const int64_t zchunk = choose_zchunk(gx * gy, nz, num_sms());  // one CTA per SM
     const int64_t gz = (nz + zchunk - 1) / zchunk;
+    Dims db = d;
+    db.band = band_width(H3_RC3_BAND);  // tile rasterisation (band_tile, h3_launch.h)
     recon_dmma3_kernel<<<dim3((unsigned)gx, (unsigned)gy, (unsigned)gz), THREADS, SMEM, st>>>(
-        src, coeff, d, off, (int)zchunk, hp, guard);
+        src, coeff, db, off, (int)zchunk, hp, guard);
     return (int)cudaGetLastError();
 }
 

@@ -19,6 +19,10 @@
 #include "h3_launch.h"
 #include "h3_tma.cuh"
 
+#ifndef H3_WS5_BAND
+#define H3_WS5_BAND 4
+#endif
+
 namespace h3 {
 namespace ws5 {
 
@@ -141,7 +145,9 @@ sep_fused_dmma_ws_kernel(const double* __restrict__ src, double* __restrict__ ds
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int q = lane & 3, g = lane >> 2;
     const int M1 = (int)d.M1, M2 = (int)d.M2;
-    const int cx0 = blockIdx.x * TX, cy0 = blockIdx.y * C::TY;
+    int tbx, tby;
+    band_tile(d.band, 1, tbx, tby);
+    const int cx0 = tbx * TX, cy0 = tby * C::TY;
     const int64_t zc0 = d.z_begin + (int64_t)blockIdx.z * zchunk;
     const int64_t zc1 = min(zc0 + (int64_t)zchunk, d.z_end);
     const int P = (int)(zc1 - zc0) + 1;  // node planes of this chunk
@@ -383,7 +389,9 @@ static int launch_ws(const double* src, double* dst, const Dims& d, const double
     if (e != cudaSuccess) return (int)e;
     const int64_t zchunk = choose_zchunk(gx * gy, nz, (int64_t)num_sms() * (per_sm > 0 ? per_sm : 1));
     const int64_t gz = (nz + zchunk - 1) / zchunk;
-    kern<<<dim3((unsigned)gx, (unsigned)gy, (unsigned)gz), C::THREADS, C::SMEM, st>>>(src, dst, d, off, (int)zchunk,
+    Dims db = d;
+    db.band = band_width(H3_WS5_BAND);  // tile rasterisation (band_tile, h3_launch.h)
+    kern<<<dim3((unsigned)gx, (unsigned)gy, (unsigned)gz), C::THREADS, C::SMEM, st>>>(src, dst, db, off, (int)zchunk,
                                                                                    ops, first_bad, guard);
     return (int)cudaGetLastError();
 }

@@ -21,6 +21,9 @@ struct Dims {
     // NVLink through a CUDA-IPC mapping); nullptr = contiguous with the field
     const double* ghost_lo = nullptr;
     const double* ghost_hi = nullptr;
+    // column-band width of the tile rasterisation (band_tile below; 0 = plain row order), set by
+    // the launchers of the tile-march kernels
+    int band = 0;
 };
 
 // Base of node plane gz of a (slab) field: the field itself, or a separately held ghost plane.
@@ -103,6 +106,9 @@ int check_finite_launch(const double* field, int64_t M1, int64_t M2, int64_t M3,
                         unsigned long long* first_bad, cudaStream_t st);
 
 int num_sms();
+
+// Band width a launcher uses: its compiled default, or (tools library only) H3_BAND.
+int band_width(int dflt);
 
 // Tile rasterisation.  The hardware starts CTAs in linear block order (x fastest), so with a plain
 // mapping the CTAs resident at one time cover ~148 / gx full tile rows: every tile on the lower

@@ -8,9 +8,23 @@
 //         node values (DOF n = 0) against sum_t e3[t][m3] e2[t][m2] e1[t][m1].
 //         Two-stage deterministic reduction (no float atomics).
 // finite: reference pipeline.py:210-215 -- first non-finite node in C order.
+#include <cstdlib>
+
 #include "h3_launch.h"
 
 namespace h3 {
+
+int band_width(int dflt) {
+#ifdef H3_MEASURE
+    static const int v = [] {  // tools library only: H3_BAND overrides every launcher's default
+        const char* e = getenv("H3_BAND");
+        return e ? atoi(e) : -1;
+    }();
+    return v >= 0 ? v : dflt;
+#else
+    return dflt;
+#endif
+}
 
 int num_sms() {
     int dev = 0, sms = 148;

@@ -20,6 +20,10 @@
 #include "h3_launch.h"
 #include "h3_tma.cuh"
 
+#ifndef H3_RWS5_BAND
+#define H3_RWS5_BAND 0
+#endif
+
 namespace h3 {
 namespace rws5 {
 
@@ -103,7 +107,9 @@ recon_dmma_ws_kernel(const double* __restrict__ src, double* __restrict__ coeff,
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int q = lane & 3, g = lane >> 2;
     const int M1 = (int)d.M1, M2 = (int)d.M2;
-    const int cx0 = blockIdx.x * TX, cy0 = blockIdx.y * C::TY;
+    int tbx, tby;
+    band_tile(d.band, 1, tbx, tby);
+    const int cx0 = tbx * TX, cy0 = tby * C::TY;
     const int64_t zc0 = d.z_begin + (int64_t)blockIdx.z * zchunk;
     const int64_t zc1 = min(zc0 + (int64_t)zchunk, d.z_end);
     const int P = (int)(zc1 - zc0) + 1;  // node planes of this chunk
@@ -381,7 +387,9 @@ static int launch_rws5(const double* src, double* coeff, const Dims& d, const do
     const int64_t gx = (d.M1 + C::TX - 1) / C::TX, gy = (d.M2 + C::TY - 1) / C::TY;
     const int64_t zchunk = choose_zchunk(gx * gy, nz, num_sms());  // one CTA per SM
     const int64_t gz = (nz + zchunk - 1) / zchunk;
-    kern<<<dim3((unsigned)gx, (unsigned)gy, (unsigned)gz), C::THREADS, C::SMEM, st>>>(src, coeff, d, off, (int)zchunk,
+    Dims db = d;
+    db.band = band_width(H3_RWS5_BAND);  // tile rasterisation (band_tile, h3_launch.h)
+    kern<<<dim3((unsigned)gx, (unsigned)gy, (unsigned)gz), C::THREADS, C::SMEM, st>>>(src, coeff, db, off, (int)zchunk,
                                                                                    hp, guard);
     return (int)cudaGetLastError();
 }

@@ -8,6 +8,7 @@
 #   FAMILY m3: m=3 fused kernels        (H3_DMMA_CFG:  10x warp-specialised, 20x x1->x2 chained)
 #          m5: m=5 fused kernels        (H3_DMMA5_CFG: lock-step shapes, 20+k warp-specialised)
 #          r5: m=5 reconstruction       (H3_RECON5_WS: warp-specialised variants)
+#          r3: m=3 two-kernel step      (H3_BAND: tile rasterisation of the reconstruction)
 # outputs: gpurun_out/TAG_{make,check,ab,prof}.txt, gpurun_out/TAG_vK.ncu-rep
 cd "$GRAFT_REPO_ROOT" 2>/dev/null || cd /root/repo
 family=$1; tag=$2; variants=$3; prof=$4
@@ -15,6 +16,7 @@ case $family in
   m3) var=H3_DMMA_CFG;  order=3; mode=fused;    tsize=512; tsteps=4; psize=256; kre=sep_fused ;;
   m5) var=H3_DMMA5_CFG; order=5; mode=fused;    tsize=256; tsteps=4; psize=128; kre=sep_fused ;;
   r5) var=H3_RECON5_WS; order=5; mode=two_pass; tsize=256; tsteps=2; psize=128; kre=recon ;;
+  r3) var=H3_BAND;      order=3; mode=two_pass; tsize=256; tsteps=4; psize=128; kre=recon ;;
   *) echo "unknown family $family"; exit 2 ;;
 esac
 mkdir -p gpurun_out
