@@ -73,7 +73,7 @@ def measured_traffic(order_n, cells, mode, variant):
     (profiles/*_summary.json), when that capture is of this exact workload."""
     if (order_n, cells, mode, variant) != (3, 512, "fused", "separable"):
         return None, None
-    p = ROOT / "profiles" / "r01_sep_fused_dmma3_512_summary.json"
+    p = ROOT / "profiles" / "r02_fused3_512_sep_fused_summary.json"
     if not p.exists():
         return None, None
     d = json.loads(p.read_text())
@@ -343,8 +343,9 @@ def main():
                      "frac": (achieved / peak_gbs) if achieved else None, "traffic": traffic,
                      "traffic_unit": "DRAM bytes per launch (ncu dram__bytes_read+write)",
                      "traffic_source": traffic_src,
-                     "kernel": ("sep_fused_dmma3_kernel (DMMA m8n8k4, 8x7 tile, 16 warps, TMA row loads, x3/x1 plane pipelining)" if order_n == 3
-                                else ("sep_fused_dmma_cp_kernel<5> (DMMA cell-pair)" if order_n == 5
+                     "kernel": ("sep_fused_dmma3_kernel (DMMA m8n8k4, 8x7 tile, 16 warps, TMA row loads, x3/x1 plane pipelining, "
+                                 "column-band tile rasterisation)" if order_n == 3
+                                else ("sep_fused_dmma_ws_kernel (DMMA cell-pair, warp-specialised)" if order_n == 5
                                       else f"sep_fused_kernel<{order_n}>")) if args.mode == "fused" else "recon+evolve",
                      "algorithmic_bytes_per_launch": alg_bytes, "mean_launch_ms": launch_ms,
                      "peak_source": peak_src},

@@ -20,7 +20,7 @@
 #include "h3_tma.cuh"
 
 #ifndef H3_WS5_BAND
-#define H3_WS5_BAND 4
+#define H3_WS5_BAND 8
 #endif
 
 namespace h3 {
