@@ -420,6 +420,8 @@ int sep_fused_dmma5_ws_launch(const double* src, double* dst, const Dims& d, con
         case 26: return launch_ws<ws5::Cfg<3, 4, 7, 6, 6, 2, 3, true, 2, 4>>(src, dst, d, A, off, st, first_bad, guard);
         case 27: return launch_ws<ws5::Cfg<2, 6, 7, 6, 6, 2, 0, true, 2, 4>>(src, dst, d, A, off, st, first_bad, guard);
         case 28: return launch_ws<ws5::Cfg<2, 6, 7, 6, 6, 2, 5, true, 2, 4>>(src, dst, d, A, off, st, first_bad, guard);
+        case 29: return launch_ws<ws5::Cfg<2, 6, 7, 6, 6, 2, 1, true, 2, 4>>(src, dst, d, A, off, st, first_bad, guard);
+        case 30: return launch_ws<ws5::Cfg<2, 6, 7, 6, 6, 2, 2, true, 2, 4>>(src, dst, d, A, off, st, first_bad, guard);
         case 17: return launch_ws<ws5::Cfg<2, 6, 8, 6, 6, 3, 3, true>>(src, dst, d, A, off, st, first_bad, guard);
         case 18: return launch_ws<ws5::Cfg<3, 4, 9, 6, 6, 3, 3, true>>(src, dst, d, A, off, st, first_bad, guard);
         case 19: return launch_ws<ws5::Cfg<2, 6, 8, 7, 7, 3, 3, true>>(src, dst, d, A, off, st, first_bad, guard);
@@ -438,9 +440,9 @@ int sep_fused_dmma5_ws_launch(const double* src, double* dst, const Dims& d, con
     (void)variant;
 #endif
     // 2 x 6 cell tiles (x1 halo rows 7/6), 7 x1 + 6 x2 + 6 x3 warps + the TMA producer, 2 TMA
-    // stages, W ring of 2, V ring of 4, 3 line groups per batch, the searched layouts:
-    // 15.3 ms per half step at 256^3 vs 17.6 ms for the lock-step kernel (r02)
-    return launch_ws<ws5::Cfg<2, 6, 7, 6, 6, 2, 3, true, 2, 4>>(src, dst, d, A, off, st, first_bad, guard);
+    // stages, W ring of 2, V ring of 4, 2 line groups per batch (3: 1 % slower), the searched
+    // layouts: 15.2 ms per half step at 256^3 vs 17.6 ms for the lock-step kernel (r02)
+    return launch_ws<ws5::Cfg<2, 6, 7, 6, 6, 2, 2, true, 2, 4>>(src, dst, d, A, off, st, first_bad, guard);
 }
 
 }  // namespace h3
