@@ -57,8 +57,11 @@ __device__ __forceinline__ unsigned exp_gap(double x) {
     return r;
 }
 
-template <int TY_, int STAGES_ = 3, int B3_ = 7, int NX3_ = 8>
+template <int TY_, int STAGES_ = 3, int B3_ = 7, int NX3_ = 8, bool SPLIT_ = false>
 struct Cfg {
+    // SPLIT: x1 of all node-row pairs first (4 independent chains, interleaved), then the two x2
+    // chains -- a shorter dependency path per plane than row pair after row pair
+    static constexpr bool SPLIT = SPLIT_;
     static constexpr int n = 4, n3 = 64;
     static constexpr int TX = 8, TY = TY_, NX = TX + 1, NY = TY + 1;
     static constexpr int NSEG = TX / 4;                 // 4-cell row segments
@@ -171,6 +174,59 @@ sep_fused_dmma3x_kernel(const double* __restrict__ src, double* __restrict__ dst
             double x2r[2][2], sv2[2][2];
 #pragma unroll
             for (int s = 0; s < 2; ++s) x2r[s][0] = x2r[s][1] = sv2[s][0] = sv2[s][1] = 0.0;
+            // x2 step of cell pair s at node row ly with A fragment xa; completed cell rows to V
+            auto x2_step = [&](int s, int ly, double xa) {
+                dmma(x2r[s][0], x2r[s][1], xa, o2[ly & 1]);
+                // x2 completion: cell row ly - 1 in the lanes with par == (ly + 1) & 1
+                if (ly & 1) {
+                    if (ly == NY - 1) {  // lone last cell row: half-warp store
+                        if (par == 0) {
+                            double* v = Vb + (ly - 1) * VROW + s * 2 * VCS;
+                            v[0] = x2r[s][0];
+                            v[16] = x2r[s][1];
+                        }
+                    } else {
+                        sv2[s][0] = x2r[s][0];
+                        sv2[s][1] = x2r[s][1];
+                    }
+                } else if (ly > 0) {
+                    // rows ly-2 (par 0, saved) and ly-1 (par 1) in one full-warp store
+                    double* v = Vb + (ly - 2 + par) * VROW + s * 2 * VCS;
+                    v[0] = par ? x2r[s][0] : sv2[s][0];
+                    v[16] = par ? x2r[s][1] : sv2[s][1];
+                }
+                const bool d2 = par == ((ly + 1) & 1);
+                x2r[s][0] = d2 ? 0.0 : x2r[s][0];
+                x2r[s][1] = d2 ? 0.0 : x2r[s][1];
+            };
+            if constexpr (C::SPLIT) {
+                constexpr int R = NY / 2;
+                double r1[R][2], sv[R][2], xd[R][2][2];
+#pragma unroll
+                for (int r = 0; r < R; ++r) r1[r][0] = r1[r][1] = sv[r][0] = sv[r][1] = 0.0;
+#pragma unroll
+                for (int k = 0; k < 5; ++k) {
+                    const bool done = hi == ((k + 1) & 1);
+#pragma unroll
+                    for (int r = 0; r < R; ++r) {
+                        dmma(r1[r][0], r1[r][1], o1[k & 1], Ub[2 * r * URS + k * n3]);
+                        if (k & 1) {
+                            sv[r][0] = r1[r][0];
+                            sv[r][1] = r1[r][1];
+                        } else if (k > 0) {
+                            const int s = (k - 2) >> 1;
+                            xd[r][s][0] = hi ? r1[r][0] : sv[r][0];
+                            xd[r][s][1] = hi ? r1[r][1] : sv[r][1];
+                        }
+                        r1[r][0] = done ? 0.0 : r1[r][0];
+                        r1[r][1] = done ? 0.0 : r1[r][1];
+                    }
+                }
+#pragma unroll
+                for (int ly = 0; ly < NY; ++ly)
+#pragma unroll
+                    for (int s = 0; s < 2; ++s) x2_step(s, ly, xd[ly >> 1][s][ly & 1]);
+            } else {
 #pragma unroll
             for (int r = 0; r < NY / 2; ++r) {
                 double a[5];
@@ -190,36 +246,12 @@ sep_fused_dmma3x_kernel(const double* __restrict__ src, double* __restrict__ dst
                         // from sv, odd cell in g >= 4): two x2 steps, node rows 2r (i = 0), 2r+1
                         const int s = (k - 2) >> 1;
 #pragma unroll
-                        for (int i = 0; i < 2; ++i) {
-                            const int ly = 2 * r + i;
-                            const double xa = hi ? r1[i] : sv[i];
-                            dmma(x2r[s][0], x2r[s][1], xa, o2[ly & 1]);
-                            // x2 completion: cell row ly - 1 in the lanes with par == (ly + 1) & 1
-                            if (ly & 1) {
-                                if (ly == NY - 1) {  // lone last cell row: half-warp store
-                                    if (par == 0) {
-                                        double* v = Vb + (ly - 1) * VROW + s * 2 * VCS;
-                                        v[0] = x2r[s][0];
-                                        v[16] = x2r[s][1];
-                                    }
-                                } else {
-                                    sv2[s][0] = x2r[s][0];
-                                    sv2[s][1] = x2r[s][1];
-                                }
-                            } else if (ly > 0) {
-                                // rows ly-2 (par 0, saved) and ly-1 (par 1) in one full-warp store
-                                double* v = Vb + (ly - 2 + par) * VROW + s * 2 * VCS;
-                                v[0] = par ? x2r[s][0] : sv2[s][0];
-                                v[16] = par ? x2r[s][1] : sv2[s][1];
-                            }
-                            const bool d2 = par == ((ly + 1) & 1);
-                            x2r[s][0] = d2 ? 0.0 : x2r[s][0];
-                            x2r[s][1] = d2 ? 0.0 : x2r[s][1];
-                        }
+                        for (int i = 0; i < 2; ++i) x2_step(s, 2 * r + i, hi ? r1[i] : sv[i]);
                     }
                     r1[0] = done ? 0.0 : r1[0];
                     r1[1] = done ? 0.0 : r1[1];
                 }
+            }
             }
         }
         __syncthreads();  // matches the x3 warps' final iteration
@@ -265,14 +297,11 @@ sep_fused_dmma3x_kernel(const double* __restrict__ src, double* __restrict__ dst
                 const bool done = (k & 1) ? !de : de;
                 dmma(acc[k][0], acc[k][1], a[k], ((t + k) & 1) ? b1 : b0);
                 if (t > 0) {
-                    // predicated streaming stores (no branch): finished lanes of live chains
-                    double* o = ob + (cyk(k) * rowstep + cxk(k) * n3);
-                    const unsigned pr = (unsigned)(done && (live >> k & 1u));
-                    asm volatile(
-                        "{\n.reg .pred p;\nsetp.ne.u32 p, %3, 0;\n"
-                        "@p st.global.cs.f64 [%0], %1;\n@p st.global.cs.f64 [%0+128], %2;\n}\n" ::"l"(o),
-                        "d"(acc[k][0]), "d"(acc[k][1]), "r"(pr)
-                        : "memory");
+                    if (done && (live >> k & 1u)) {  // finished lanes of live chains
+                        double* o = ob + (cyk(k) * rowstep + cxk(k) * n3);
+                        __stcs(o, acc[k][0]);
+                        __stcs(o + 16, acc[k][1]);
+                    }
                     screen = min(screen, min(exp_gap(acc[k][0]), exp_gap(acc[k][1])));
                 }
                 acc[k][0] = done ? 0.0 : acc[k][0];
@@ -337,6 +366,9 @@ int sep_fused_dmma3x_launch(const double* src, double* dst, const Dims& d, const
         case 3: return launch_x12<Cfg<7, 3, 4, 16>>(src, dst, d, ops, off, st, first_bad, guard, 2);
         case 4: return launch_x12<Cfg<7, 3, 2, 8>>(src, dst, d, ops, off, st, first_bad, guard, 2);
         case 5: return launch_x12<Cfg<7, 3, 7, 16>>(src, dst, d, ops, off, st, first_bad, guard, 1);
+        case 6: return launch_x12<Cfg<7, 3, 7, 16, true>>(src, dst, d, ops, off, st, first_bad, guard, 2);
+        case 7: return launch_x12<Cfg<7, 4, 7, 16, true>>(src, dst, d, ops, off, st, first_bad, guard, 2);
+        case 8: return launch_x12<Cfg<7, 3, 7, 8, true>>(src, dst, d, ops, off, st, first_bad, guard, 2);
         default: break;
     }
     return launch_x12<Cfg<7, 3, 7>>(src, dst, d, ops, off, st, first_bad, guard, 2);
