@@ -64,8 +64,12 @@ using tma::mbar_wait;
 // ABL (measurement-only ablations, results are garbage): bit 0 skips the global stores,
 // bit 1 the input copies, bit 2 replaces every DMMA by a register update.
 template <int TY_, int WARPS_, int STAGES_, bool VALIAS_, int MINB_ = 1, int ABL_ = 0, bool TMA_ = false,
-          bool LEAN_ = false, int PIPE_ = 0, bool CF_ = false>
+          bool LEAN_ = false, int PIPE_ = 0, bool CF_ = false, bool FI_ = false>
 struct Dm3Cfg {
+    // FI: the per-plane TMA issue and mbarrier wait use shared addresses, source offsets and the
+    // periodic-wrap split of the tile row precomputed once per CTA (the loader lanes' issue sits on
+    // the path between the two CTA barriers of a plane)
+    static constexpr bool FI = FI_;
     // CF: W cell stride 84 and an odd V row stride, so the paired stores of x1 / x2 (the two lane
     // halves write neighbouring cells / cell rows) hit distinct banks (80 and 8 x 68 are 0 mod 16)
     static constexpr bool CF = CF_;
@@ -178,8 +182,39 @@ sep_fused_dmma3_kernel(const double* __restrict__ src, double* __restrict__ dst,
     // node plane of the next copy, wrapped incrementally
     int64_t gz_next = d.periodic_z ? wrap(zc0 + off, d.M3) : zc0 + off;
     int issued = 0;
+    // FI: precomputed loader state (lane 0 of warp < NY): tile row split at the periodic wrap into
+    // at most two bulk copies, their shared destinations in stage 0, the barrier address
+    const uint32_t bar_u32 = smem_u32(bars);
+    uint32_t sdst0 = 0, bytes1 = 0, bytes2 = 0;
+    int64_t soff1 = 0, soff2 = 0;
+    if constexpr (C::FI) {
+        if (lane == 0 && warp < NY) {
+            const int len1 = min(NX, M1 - gx0);
+            sdst0 = smem_u32(U + warp * NX * UNS);
+            soff1 = ((int64_t)rowoff + gx0) * n3;
+            soff2 = (int64_t)rowoff * n3;
+            bytes1 = (unsigned)(len1 * UNS * sizeof(double));
+            bytes2 = (unsigned)((NX - len1) * UNS * sizeof(double));
+        }
+    }
     auto issue = [&]() {
-        if constexpr (C::TMA) {
+        if constexpr (C::TMA && C::FI) {
+            if (issued < P) {
+                if (lane == 0 && warp < NY) {
+                    const int s = issued % STAGES;
+                    const uint32_t bar = bar_u32 + 8u * (unsigned)s;
+                    const uint32_t sd = sdst0 + (uint32_t)(s * C::U_D * sizeof(double));
+                    fence_proxy_async_smem();
+                    if (warp == 0) tma::mbar_arrive_expect_tx_u32(bar, (unsigned)(NCOL * UNS * sizeof(double)));
+                    const double* base = plane_base(src, gz_next, plane_elems, d);
+                    tma::bulk_g2s_u32(sd, base + soff1, bytes1, bar);
+                    if (bytes2) tma::bulk_g2s_u32(sd + bytes1, base + soff2, bytes2, bar);
+                }
+                ++gz_next;
+                if (d.periodic_z && gz_next == d.M3) gz_next = 0;
+                ++issued;
+            }
+        } else if constexpr (C::TMA) {
             if (issued < P) {
                 // lane 0 of warp ly < NY copies tile row ly; warp 0 also posts the byte count
                 // (the mbarrier tx-count may run ahead of it: the phase cannot complete before
@@ -424,7 +459,10 @@ sep_fused_dmma3_kernel(const double* __restrict__ src, double* __restrict__ dst,
         if constexpr (C::TMA) {
             __syncthreads();
             issue();  // the stage it fills was last read before the barrier above
-            if (!(C::ABL & 2)) mbar_wait(&bars[pl % STAGES], (unsigned)((pl / STAGES) & 1));
+            if constexpr (C::FI)
+                tma::mbar_wait_u32(bar_u32 + 8u * (unsigned)(pl % STAGES), (unsigned)((pl / STAGES) & 1));
+            else if (!(C::ABL & 2))
+                mbar_wait(&bars[pl % STAGES], (unsigned)((pl / STAGES) & 1));
         } else {
             cp_async_wait<STAGES - 2>();
             __syncthreads();
@@ -458,9 +496,6 @@ sep_fused_dmma3_kernel(const double* __restrict__ src, double* __restrict__ dst,
 // column-band widths of the tile rasterisation (band_tile, h3_launch.h)
 #ifndef H3_DMMA3_BAND
 #define H3_DMMA3_BAND 8
-#endif
-#ifndef H3_RC3_BAND
-#define H3_RC3_BAND 0
 #endif
 
 template <class C>
@@ -549,6 +584,7 @@ int sep_fused_dmma3_launch(const double* src, double* dst, const Dims& d, const 
         case 15: return launch_dm3<Dm3Cfg<7, 16, 3, true, 1, 5, true>>(src, dst, d, ops, off, st, first_bad, guard);
         case 16: return launch_dm3<Dm3Cfg<7, 16, 3, true, 1, 0, true>>(src, dst, d, ops, off, st, first_bad, guard);
         case 31: return launch_dm3<Dm3Cfg<7, 16, 3, false, 1, 0, true, true, 1, false>>(src, dst, d, ops, off, st, first_bad, guard);  // bank-conflicted W/V
+        case 32: return launch_dm3<Dm3Cfg<7, 16, 3, false, 1, 0, true, true, 1, true, true>>(src, dst, d, ops, off, st, first_bad, guard);  // precomputed issue
         default: break;
     }
 #endif
@@ -603,9 +639,7 @@ recon_dmma3_kernel(const double* __restrict__ src, double* __restrict__ coeff, D
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int q = lane & 3, g = lane >> 2;
     const int M1 = (int)d.M1, M2 = (int)d.M2;
-    int tbx, tby;
-    band_tile(d.band, 1, tbx, tby);
-    const int cx0 = tbx * TX, cy0 = tby * TY;
+    const int cx0 = blockIdx.x * TX, cy0 = blockIdx.y * TY;
     const int64_t zc0 = d.z_begin + (int64_t)blockIdx.z * zchunk;
     const int64_t zc1 = min(zc0 + (int64_t)zchunk, d.z_end);
     const int P = (int)(zc1 - zc0) + 1;
@@ -768,10 +802,10 @@ int recon_dmma3_launch(const double* src, double* coeff, const Dims& d, const do
     const int64_t gx = (d.M1 + TX - 1) / TX, gy = (d.M2 + TY - 1) / TY;
     const int64_t zchunk = choose_zchunk(gx * gy, nz, num_sms());  // one CTA per SM
     const int64_t gz = (nz + zchunk - 1) / zchunk;
-    Dims db = d;
-    db.band = band_width(H3_RC3_BAND);  // tile rasterisation (band_tile, h3_launch.h)
+    // (plain row order: the band rasterisation measured neutral to slightly slower here,
+    // profiles/r02_band_rasterisation.txt)
     recon_dmma3_kernel<<<dim3((unsigned)gx, (unsigned)gy, (unsigned)gz), THREADS, SMEM, st>>>(
-        src, coeff, db, off, (int)zchunk, hp, guard);
+        src, coeff, d, off, (int)zchunk, hp, guard);
     return (int)cudaGetLastError();
 }
 

@@ -269,17 +269,15 @@ static int sep_fused_n(const double* src, double* dst, const Dims& d, const doub
 
 // H3_FUSED_IMPL=dfma runs the DFMA kernel at N = 3, 5 too: only in the tools library
 // (-DH3_MEASURE), which backs the "DMMA only where ncu shows compute-bound" comparison.
-static bool use_dfma_ab() {
 #ifdef H3_MEASURE
+static bool use_dfma_ab() {
     static const bool v = [] {
         const char* e = getenv("H3_FUSED_IMPL");
         return e && strcmp(e, "dfma") == 0;
     }();
     return v;
-#else
-    return false;
-#endif
 }
+#endif
 
 int sep_fused_launch(const double* src, double* dst, const Dims& d, int order_n, const double* A,
                      int off, cudaStream_t st, unsigned long long* first_bad,
@@ -290,12 +288,16 @@ int sep_fused_launch(const double* src, double* dst, const Dims& d, int order_n,
         case 2: return sep_fused_n<2>(src, dst, d, A, off, st, first_bad, guard);
         case 3:
             // FP64 tensor-core kernel (h3_dmma.cu); the DFMA kernel is the tools library's A/B
+#ifdef H3_MEASURE
             if (use_dfma_ab()) return sep_fused_n<3>(src, dst, d, A, off, st, first_bad, guard);
+#endif
             return sep_fused_dmma3_launch(src, dst, d, A, off, st, first_bad, guard);
         case 4: return sep_fused_n<4>(src, dst, d, A, off, st, first_bad, guard);
         case 5:
             // FP64 tensor-core cell-pair kernel (h3_dmma5.cu)
+#ifdef H3_MEASURE
             if (use_dfma_ab()) return sep_fused_n<5>(src, dst, d, A, off, st, first_bad, guard);
+#endif
             return sep_fused_dmma5_launch(src, dst, d, A, off, st, first_bad, guard);
     }
     return (int)cudaErrorInvalidValue;
