@@ -584,6 +584,7 @@ int sep_fused_dmma3_launch(const double* src, double* dst, const Dims& d, const 
         case 15: return launch_dm3<Dm3Cfg<7, 16, 3, true, 1, 5, true>>(src, dst, d, ops, off, st, first_bad, guard);
         case 16: return launch_dm3<Dm3Cfg<7, 16, 3, true, 1, 0, true>>(src, dst, d, ops, off, st, first_bad, guard);
         case 31: return launch_dm3<Dm3Cfg<7, 16, 3, false, 1, 0, true, true, 1, false>>(src, dst, d, ops, off, st, first_bad, guard);  // bank-conflicted W/V
+        case 33: return launch_dm3<Dm3Cfg<7, 8, 3, false, 1, 0, true, true, 1, true, true>>(src, dst, d, ops, off, st, first_bad, guard);  // 8 warps, 2 tasks each
         case 32: return launch_dm3<Dm3Cfg<7, 16, 3, false, 1, 0, true, true, 1, true, true>>(src, dst, d, ops, off, st, first_bad, guard);  // precomputed issue
         default: break;
     }

@@ -422,6 +422,14 @@ int sep_fused_dmma5_ws_launch(const double* src, double* dst, const Dims& d, con
         case 28: return launch_ws<ws5::Cfg<2, 6, 7, 6, 6, 2, 5, true, 2, 4>>(src, dst, d, A, off, st, first_bad, guard);
         case 29: return launch_ws<ws5::Cfg<2, 6, 7, 6, 6, 2, 1, true, 2, 4>>(src, dst, d, A, off, st, first_bad, guard);
         case 30: return launch_ws<ws5::Cfg<2, 6, 7, 6, 6, 2, 2, true, 2, 4>>(src, dst, d, A, off, st, first_bad, guard);
+        // more x3 warps: the r02 ncu capture shows x1 and x2 waiting on their "empty" barriers
+        // (343M / 304M retries) and x3 rarely waiting -- x3 paces the pipeline
+        case 32: return launch_ws<ws5::Cfg<2, 6, 7, 6, 7, 2, 2, true, 2, 4>>(src, dst, d, A, off, st, first_bad, guard);
+        case 33: return launch_ws<ws5::Cfg<2, 6, 7, 5, 7, 2, 2, true, 2, 4>>(src, dst, d, A, off, st, first_bad, guard);
+        case 34: return launch_ws<ws5::Cfg<2, 6, 6, 6, 7, 2, 2, true, 2, 4>>(src, dst, d, A, off, st, first_bad, guard);
+        case 35: return launch_ws<ws5::Cfg<2, 6, 7, 6, 8, 2, 2, true, 2, 4>>(src, dst, d, A, off, st, first_bad, guard);
+        case 36: return launch_ws<ws5::Cfg<2, 6, 7, 7, 7, 2, 2, true, 2, 4>>(src, dst, d, A, off, st, first_bad, guard);
+        case 37: return launch_ws<ws5::Cfg<2, 6, 7, 6, 9, 2, 2, true, 2, 4>>(src, dst, d, A, off, st, first_bad, guard);
         case 17: return launch_ws<ws5::Cfg<2, 6, 8, 6, 6, 3, 3, true>>(src, dst, d, A, off, st, first_bad, guard);
         case 18: return launch_ws<ws5::Cfg<3, 4, 9, 6, 6, 3, 3, true>>(src, dst, d, A, off, st, first_bad, guard);
         case 19: return launch_ws<ws5::Cfg<2, 6, 8, 7, 7, 3, 3, true>>(src, dst, d, A, off, st, first_bad, guard);
@@ -439,10 +447,11 @@ int sep_fused_dmma5_ws_launch(const double* src, double* dst, const Dims& d, con
 #else
     (void)variant;
 #endif
-    // 2 x 6 cell tiles (x1 halo rows 7/6), 7 x1 + 6 x2 + 6 x3 warps + the TMA producer, 2 TMA
-    // stages, W ring of 2, V ring of 4, 2 line groups per batch (3: 1 % slower), the searched
-    // layouts: 15.2 ms per half step at 256^3 vs 17.6 ms for the lock-step kernel (r02)
-    return launch_ws<ws5::Cfg<2, 6, 7, 6, 6, 2, 2, true, 2, 4>>(src, dst, d, A, off, st, first_bad, guard);
+    // 2 x 6 cell tiles (x1 halo rows 7/6), 7 x1 + 6 x2 + 7 x3 warps + the TMA producer (x3 paces
+    // the pipeline: 6 x3 warps 1 % slower), 2 TMA stages, W ring of 2, V ring of 4, 2 line groups
+    // per batch (3: 1 % slower), the searched layouts: 14.8 ms per half step at 256^3 vs 17.6 ms
+    // for the lock-step kernel (r02)
+    return launch_ws<ws5::Cfg<2, 6, 7, 6, 7, 2, 2, true, 2, 4>>(src, dst, d, A, off, st, first_bad, guard);
 }
 
 }  // namespace h3
