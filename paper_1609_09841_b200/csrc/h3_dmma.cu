@@ -626,6 +626,7 @@ __device__ __forceinline__ int wpos(int i1, int j2) { return 4 * (i1 + (i1 >> 2)
 __device__ __forceinline__ int vpos(int i2, int i1, int j3) { return (i2 * 8 + i1) * 4 + ((j3 + (i2 >> 1)) & 3); }
 }  // namespace rc3
 
+template <bool PIPE>
 __global__ void __launch_bounds__(rc3::THREADS, 1)
 recon_dmma3_kernel(const double* __restrict__ src, double* __restrict__ coeff, Dims d, int off,
                    int zchunk, const __grid_constant__ LitOps<double, 3> hp,
@@ -688,12 +689,11 @@ recon_dmma3_kernel(const double* __restrict__ src, double* __restrict__ coeff, D
 #pragma unroll
     for (int k = 0; k < K3; ++k) acc[k][0] = acc[k][1] = 0.0;
 
-    for (int pl = 0; pl < P; ++pl) {
-        cp_async_wait<STAGES - 2>();
-        __syncthreads();
-        issue();
-        const double* Ub = U + (pl % STAGES) * U_D;
-
+    // the three passes of one node plane; PIPE runs x3 of plane p-1 in the barrier interval of x1
+    // of plane p (2 barriers per plane instead of 3, and the warps without an x1 task -- 10 tasks
+    // for 16 warps -- start on x3 at once); single W and V buffers suffice: V(p-1) is read in the
+    // interval before x2(p) rewrites it, W(p) is written after x2(p-1) read it
+    auto x1_pass = [&](const double* Ub) {
         // ---- x1: (row, line group) chains along x1 -----------------------------------------
         if (warp < T1) {
             const int ly = warp >> 1, G = warp & 1;
@@ -718,8 +718,8 @@ recon_dmma3_kernel(const double* __restrict__ src, double* __restrict__ coeff, D
                 }
             }
         }
-        __syncthreads();
-
+    };
+    auto x2_pass = [&]() {
         // ---- x2: (column, j3) chains along x2 ------------------------------------------------
 #pragma unroll
         for (int j = 0; j < K2; ++j) {
@@ -746,8 +746,8 @@ recon_dmma3_kernel(const double* __restrict__ src, double* __restrict__ coeff, D
                 }
             }
         }
-        __syncthreads();
-
+    };
+    auto x3_pass = [&](const int pl) {
         // ---- x3: chains across planes; completed cell planes go straight to HBM ----------------
         {
             const int64_t plane_off = (int64_t)(pl - 1) * cplane;
@@ -783,9 +783,39 @@ recon_dmma3_kernel(const double* __restrict__ src, double* __restrict__ coeff, D
                 }
             }
         }
+        };
+    if constexpr (PIPE) {
+        for (int pl = 0; pl <= P; ++pl) {
+            if (pl < P) {
+                cp_async_wait<STAGES - 2>();
+                __syncthreads();
+                issue();
+            } else {
+                __syncthreads();
+            }
+            if (pl >= 1) x3_pass(pl - 1);
+            if (pl < P) x1_pass(U + (pl % STAGES) * U_D);
+            __syncthreads();
+            if (pl < P) x2_pass();
+        }
+    } else {
+        for (int pl = 0; pl < P; ++pl) {
+            cp_async_wait<STAGES - 2>();
+            __syncthreads();
+            issue();
+            x1_pass(U + (pl % STAGES) * U_D);
+            __syncthreads();
+            x2_pass();
+            __syncthreads();
+            x3_pass(pl);
+        }
     }
     cp_async_wait<0>();
 }
+
+#ifndef H3_RC3_PIPE_DEFAULT
+#define H3_RC3_PIPE_DEFAULT false
+#endif
 
 int recon_dmma3_launch(const double* src, double* coeff, const Dims& d, const double* h_mat, int off,
                        cudaStream_t st, const unsigned long long* guard) {
@@ -798,14 +828,23 @@ int recon_dmma3_launch(const double* src, double* coeff, const Dims& d, const do
     for (int i = 0; i < 8; ++i) hp.f1[i] = hp.f2[i] = hp.f3[i] = 0.0;
     for (int i = 0; i < H3_MAX_STAGES; ++i) hp.cf[i] = 0.0;
     hp.q = 0;
-    cudaError_t e = cudaFuncSetAttribute(recon_dmma3_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM);
+#ifdef H3_MEASURE
+    static const bool pipe = [] {  // tools library only: H3_RC3_PIPE=0/1
+        const char* e = getenv("H3_RC3_PIPE");
+        return e ? atoi(e) != 0 : H3_RC3_PIPE_DEFAULT;
+    }();
+#else
+    constexpr bool pipe = H3_RC3_PIPE_DEFAULT;
+#endif
+    auto kern = pipe ? recon_dmma3_kernel<true> : recon_dmma3_kernel<false>;
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM);
     if (e != cudaSuccess) return (int)e;
     const int64_t gx = (d.M1 + TX - 1) / TX, gy = (d.M2 + TY - 1) / TY;
     const int64_t zchunk = choose_zchunk(gx * gy, nz, num_sms());  // one CTA per SM
     const int64_t gz = (nz + zchunk - 1) / zchunk;
     // (plain row order: the band rasterisation measured neutral to slightly slower here,
     // profiles/r02_band_rasterisation.txt)
-    recon_dmma3_kernel<<<dim3((unsigned)gx, (unsigned)gy, (unsigned)gz), THREADS, SMEM, st>>>(
+    kern<<<dim3((unsigned)gx, (unsigned)gy, (unsigned)gz), THREADS, SMEM, st>>>(
         src, coeff, d, off, (int)zchunk, hp, guard);
     return (int)cudaGetLastError();
 }
