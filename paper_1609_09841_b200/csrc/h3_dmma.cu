@@ -814,7 +814,8 @@ recon_dmma3_kernel(const double* __restrict__ src, double* __restrict__ coeff, D
 }
 
 #ifndef H3_RC3_PIPE_DEFAULT
-#define H3_RC3_PIPE_DEFAULT false
+// x3 of plane p-1 pipelined with x1 of plane p: 0.7 % faster m=3 two-kernel step (r02)
+#define H3_RC3_PIPE_DEFAULT true
 #endif
 
 int recon_dmma3_launch(const double* src, double* coeff, const Dims& d, const double* h_mat, int off,
@@ -833,10 +834,10 @@ int recon_dmma3_launch(const double* src, double* coeff, const Dims& d, const do
         const char* e = getenv("H3_RC3_PIPE");
         return e ? atoi(e) != 0 : H3_RC3_PIPE_DEFAULT;
     }();
-#else
-    constexpr bool pipe = H3_RC3_PIPE_DEFAULT;
-#endif
     auto kern = pipe ? recon_dmma3_kernel<true> : recon_dmma3_kernel<false>;
+#else
+    auto kern = recon_dmma3_kernel<H3_RC3_PIPE_DEFAULT>;
+#endif
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM);
     if (e != cudaSuccess) return (int)e;
     const int64_t gx = (d.M1 + TX - 1) / TX, gy = (d.M2 + TY - 1) / TY;
