@@ -844,7 +844,7 @@ int recon_dmma3_launch(const double* src, double* coeff, const Dims& d, const do
     const int64_t zchunk = choose_zchunk(gx * gy, nz, num_sms());  // one CTA per SM
     const int64_t gz = (nz + zchunk - 1) / zchunk;
     // (plain row order: the band rasterisation measured neutral to slightly slower here,
-    // profiles/r02_band_rasterisation.txt)
+    // profiles/r02_tuning_ab.txt)
     kern<<<dim3((unsigned)gx, (unsigned)gy, (unsigned)gz), THREADS, SMEM, st>>>(
         src, coeff, d, off, (int)zchunk, hp, guard);
     return (int)cudaGetLastError();
