@@ -189,12 +189,15 @@ sep_fused_dmma3_kernel(const double* __restrict__ src, double* __restrict__ dst,
     int64_t soff1 = 0, soff2 = 0;
     if constexpr (C::FI) {
         if (lane == 0 && warp < NY) {
-            const int len1 = min(NX, M1 - gx0);
+            // a row narrower than the tile (M1 < NX) wraps more than once: the second piece is
+            // clamped to the row (columns 0 .. gx0, all the in-grid cells need); the node slots
+            // past it belong to out-of-grid cells only, whose outputs are never stored
+            const int len1 = min(NX, M1 - gx0), len2 = min(NX - len1, M1);
             sdst0 = smem_u32(U + warp * NX * UNS);
             soff1 = ((int64_t)rowoff + gx0) * n3;
             soff2 = (int64_t)rowoff * n3;
             bytes1 = (unsigned)(len1 * UNS * sizeof(double));
-            bytes2 = (unsigned)((NX - len1) * UNS * sizeof(double));
+            bytes2 = (unsigned)(len2 * UNS * sizeof(double));
         }
     }
     auto issue = [&]() {
@@ -205,7 +208,8 @@ sep_fused_dmma3_kernel(const double* __restrict__ src, double* __restrict__ dst,
                     const uint32_t bar = bar_u32 + 8u * (unsigned)s;
                     const uint32_t sd = sdst0 + (uint32_t)(s * C::U_D * sizeof(double));
                     fence_proxy_async_smem();
-                    if (warp == 0) tma::mbar_arrive_expect_tx_u32(bar, (unsigned)(NCOL * UNS * sizeof(double)));
+                    // every loader row copies the same bytes1 + bytes2 (same gx0)
+                    if (warp == 0) tma::mbar_arrive_expect_tx_u32(bar, (unsigned)NY * (bytes1 + bytes2));
                     const double* base = plane_base(src, gz_next, plane_elems, d);
                     tma::bulk_g2s_u32(sd, base + soff1, bytes1, bar);
                     if (bytes2) tma::bulk_g2s_u32(sd + bytes1, base + soff2, bytes2, bar);
