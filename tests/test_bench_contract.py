@@ -74,3 +74,15 @@ def test_bench_two_ranks_under_torchrun(halo, mode):
     assert line["config"]["halo"].startswith("p2p" if halo == "p2p" else "nccl")
     assert line["roofline"]["frac"] > 0
     assert "e2e" in line and (line["e2e"]["value"] or line["e2e"].get("error"))
+
+
+@pytest.mark.gpu
+def test_bench_strong_scaling_under_torchrun():
+    """`--strong M` (configs[4]'s 1024^3 split over the ranks): one global grid divided into x3
+    slabs, reported as strong scaling with the global cell count; exercised small on one GPU."""
+    out = _torchrun(2, "--backend", "gloo", "--strong", "48", "--steps", "2", "--warmup", "3", "--no-extras",
+                    "--no-e2e", "--halo", "auto")
+    assert out.returncode == 0, out.stderr[-3000:]
+    (line,) = _json_lines(out.stdout)
+    assert line["n_gpus"] == 2 and line["value"] > 0 and line["finite"] and line["scaling"] == "strong"
+    assert line["config"]["global_cells"] == [48, 48, 48]
