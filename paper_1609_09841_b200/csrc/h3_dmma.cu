@@ -41,7 +41,10 @@ __device__ __forceinline__ void dmma884(double& d0, double& d1, double a, double
 
 template <int ABL>
 __device__ __forceinline__ void dmma_abl(double& d0, double& d1, double a, double b) {
-    if constexpr (ABL & 4) {
+    if constexpr (ABL & 8) {  // energy ablation: the same dependencies through integer XORs only
+        d0 = __longlong_as_double(__double_as_longlong(d0) ^ __double_as_longlong(a));
+        d1 = __longlong_as_double(__double_as_longlong(d1) ^ __double_as_longlong(b));
+    } else if constexpr (ABL & 4) {
         d0 += a;
         d1 -= b;
     } else {
@@ -62,7 +65,8 @@ using tma::mbar_wait;
 // the periodic wrap) issued by lane 0 of warps 0..NY-1 and tracked by an mbarrier per stage, instead
 // of 16-B cp.async by every thread (which cost ~50 address instructions per warp per plane).
 // ABL (measurement-only ablations, results are garbage): bit 0 skips the global stores,
-// bit 1 the input copies, bit 2 replaces every DMMA by a register update.
+// bit 1 the input copies, bit 2 replaces every DMMA by a register update (two DADDs), bit 3 by
+// two 64-bit integer XORs (same dependencies, no floating-point work: the energy ablation).
 template <int TY_, int WARPS_, int STAGES_, bool VALIAS_, int MINB_ = 1, int ABL_ = 0, bool TMA_ = false,
           bool LEAN_ = false, int PIPE_ = 0, bool CF_ = false, bool FI_ = false>
 struct Dm3Cfg {
@@ -589,6 +593,9 @@ int sep_fused_dmma3_launch(const double* src, double* dst, const Dims& d, const 
         case 16: return launch_dm3<Dm3Cfg<7, 16, 3, true, 1, 0, true>>(src, dst, d, ops, off, st, first_bad, guard);
         case 31: return launch_dm3<Dm3Cfg<7, 16, 3, false, 1, 0, true, true, 1, false>>(src, dst, d, ops, off, st, first_bad, guard);  // bank-conflicted W/V
         case 33: return launch_dm3<Dm3Cfg<7, 8, 3, false, 1, 0, true, true, 1, true, true>>(src, dst, d, ops, off, st, first_bad, guard);  // 8 warps, 2 tasks each
+        case 34: return launch_dm3<Dm3Cfg<7, 16, 3, false, 1, 8, true, true, 1, true, true>>(src, dst, d, ops, off, st, first_bad, guard);  // product with XOR for DMMA (energy ablation)
+        case 35: return launch_dm3<Dm3Cfg<7, 16, 3, false, 1, 1, true, true, 1, true, true>>(src, dst, d, ops, off, st, first_bad, guard);  // product without the global stores
+        case 36: return launch_dm3<Dm3Cfg<7, 16, 3, false, 1, 9, true, true, 1, true, true>>(src, dst, d, ops, off, st, first_bad, guard);  // neither
         case 32: return launch_dm3<Dm3Cfg<7, 16, 3, false, 1, 0, true, true, 1, true, true>>(src, dst, d, ops, off, st, first_bad, guard);  // precomputed issue
         default: break;
     }
