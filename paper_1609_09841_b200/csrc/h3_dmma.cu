@@ -596,6 +596,10 @@ int sep_fused_dmma3_launch(const double* src, double* dst, const Dims& d, const 
         case 34: return launch_dm3<Dm3Cfg<7, 16, 3, false, 1, 8, true, true, 1, true, true>>(src, dst, d, ops, off, st, first_bad, guard);  // product with XOR for DMMA (energy ablation)
         case 35: return launch_dm3<Dm3Cfg<7, 16, 3, false, 1, 1, true, true, 1, true, true>>(src, dst, d, ops, off, st, first_bad, guard);  // product without the global stores
         case 36: return launch_dm3<Dm3Cfg<7, 16, 3, false, 1, 9, true, true, 1, true, true>>(src, dst, d, ops, off, st, first_bad, guard);  // neither
+        // taller tiles (fewer halo DMMAs: 6.72 / 6.64 vs 6.86 per cell) with 2 TMA stages to fit 227 KB
+        case 37: return launch_dm3<Dm3Cfg<9, 16, 2, false, 1, 0, true, true, 1, true, true>>(src, dst, d, ops, off, st, first_bad, guard);
+        case 38: return launch_dm3<Dm3Cfg<11, 16, 2, false, 1, 0, true, true, 1, true, true>>(src, dst, d, ops, off, st, first_bad, guard);
+        case 39: return launch_dm3<Dm3Cfg<7, 16, 2, false, 1, 0, true, true, 1, true, true>>(src, dst, d, ops, off, st, first_bad, guard);
         case 32: return launch_dm3<Dm3Cfg<7, 16, 3, false, 1, 0, true, true, 1, true, true>>(src, dst, d, ops, off, st, first_bad, guard);  // precomputed issue
         default: break;
     }
