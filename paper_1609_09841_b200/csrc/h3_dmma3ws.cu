@@ -21,7 +21,7 @@
 // barrier).  Every lane of a releasing role arrives (counts 32 x warps), so each lane's own
 // shared-memory accesses are ordered by its own release.
 // Measurement-only (tools build, -DH3_MEASURE): measured slower than the lock-step kernel, see
-// profiles/r02_m3_ws_variants.txt; the product library does not contain it.
+// profiles/r02_m3_fused_variants.txt; the product library does not contain it.
 #ifdef H3_MEASURE
 #include "h3_launch.h"
 #include "h3_tma.cuh"

@@ -29,7 +29,7 @@
 // tile rows are padded to 584 doubles so the two node rows of an x1 fragment hit disjoint bank
 // halves.
 // Measurement-only (tools build, -DH3_MEASURE): measured slower than the lock-step kernel, see
-// profiles/r02_m3_ws_variants.txt; the product library does not contain it.
+// profiles/r02_m3_fused_variants.txt; the product library does not contain it.
 #ifdef H3_MEASURE
 #include "h3_launch.h"
 #include "h3_tma.cuh"
