@@ -256,9 +256,10 @@ def test_timings_recorded():
     assert t["monolithic"] > 0 and t["reconstruction"] > 0 and t["evolution"] > 0
 
 
-def test_slab_range_and_ghost_planes():
-    """periodic_z=0 with explicit ghost planes == periodic field (the multi-GPU contract)."""
-    n, cells = 3, (9, 7, 10)
+@pytest.mark.parametrize("n,cells", [(3, (9, 7, 10)), (5, (5, 13, 10)), (1, (9, 7, 10))])
+def test_slab_range_and_ghost_planes(n, cells):
+    """periodic_z=0 with explicit ghost planes == periodic field (the multi-GPU contract), for the
+    DMMA N=3 kernel, the warp-specialised N=5 kernel and a DFMA order."""
     m1, m2, m3 = cells
     host = rm.init_field(rm.plane_wave_terms(), cells, (1.0, 1.0, 1.0), n)
     grid = hb.GridSpec(cells)
@@ -267,24 +268,27 @@ def test_slab_range_and_ghost_planes():
     full_src = hb.DofField(grid, n, host)
     for off, parity in ((0, "primary"), (-1, "dual")):
         src = hb.DofField(grid.with_parity(parity), n, host)
-        ref = hb.DofField.zeros(grid.with_parity("dual" if parity == "primary" else "primary"), n)
-        hb.half_step(src, ref, hb.StepConfig(variant="separable"), ops, dt=dt)
-        for variant in (1, 2):
+        for name in ("literal", "separable"):
+            variant = _native.VARIANTS[name]
+            # the same kernel on the periodic field is the reference for the slab
+            ref = hb.DofField.zeros(grid.with_parity("dual" if parity == "primary" else "primary"), n)
+            hb.half_step(src, ref, hb.StepConfig(variant=name), ops, dt=dt)
             # a slab of planes [3, 7) with one ghost plane on each side
             z0, z1 = 3, 7
             slab = torch.from_numpy(np.ascontiguousarray(host[z0 - 1:z1 + 1])).cuda()
             out = torch.zeros((z1 - z0, m2, m1, n + 1, n + 1, n + 1), dtype=torch.float64, device="cuda")
-            h_mat, f1, f2, f3, cf = rm.factor_arrays(n, cells, (1.0, 1.0, 1.0), dt / 2, 21)
+            q = 3 * (2 * n + 1)
+            h_mat, f1, f2, f3, cf = rm.factor_arrays(n, cells, (1.0, 1.0, 1.0), dt / 2, q)
             p = lambda a: a.ctypes.data_as(ctypes.c_void_p)
             plane = m2 * m1 * (n + 1) ** 3 * 8
             rc = _native.lib().h3_fused_pass(ctypes.c_void_p(slab.data_ptr() + plane), ctypes.c_void_p(out.data_ptr()),
-                                             m1, m2, z1 - z0, n, p(h_mat), p(f1), p(f2), p(f3), p(cf), 21, off,
+                                             m1, m2, z1 - z0, n, p(h_mat), p(f1), p(f2), p(f3), p(cf), q, off,
                                              0, z1 - z0, 0, variant, None, None, None)
             assert rc == 0
             torch.cuda.synchronize()
             got = out.cpu().numpy()
             want = ref.data[z0:z1]
-            assert rm.rel_err(got, want) <= 1e-11
+            assert np.array_equal(got, want), f"N={n} {name} off={off}: {rm.rel_err(got, want):.3e}"
     del full_src
 
 
