@@ -11,9 +11,10 @@
 // The reconstruction is DMMA-bound (202 DMMAs per cell against 15.6 KB of HBM traffic: 810 pipe
 // cycles vs ~690 memory cycles per cell per SM at 1.96 GHz); the lock-step kernel keeps the DMMA
 // pipe ~70 % busy because every CTA barrier drains it; here the three passes of consecutive planes
-// overlap (77 %, profiles/r02_two5_128_recon_dmma_ws_summary.json).  Layouts: x1 reads K in the searched conflict-free order of the fused kernel; the V
-// ring stride is 8 (mod 16) doubles so the x3 k-steps that straddle V(c) and V(c+1) stay on distinct
-// bank pairs (tools/rcp5_ws_layout_search.py).
+// overlap (77 %, profiles/r02_two5_128_recon_dmma_ws_summary.json).  Layouts: x1 reads K in the
+// searched conflict-free order of the fused kernel; the V ring stride is 8 (mod 16) doubles so the
+// x3 k-steps that straddle V(c) and V(c+1) stay on distinct bank pairs
+// (tools/rcp5_ws_layout_search.py).
 //
 // Phases as in h3_dmma5ws.cu: "full" waits use parity (use / ring) & 1, first "empty" waits pass at
 // once; every lane of a releasing role arrives.
