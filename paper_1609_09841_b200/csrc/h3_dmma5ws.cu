@@ -11,7 +11,9 @@
 // input is ready and its output buffer is free: x1 of plane t, x2 of plane t-1 and x3 of cell plane
 // t-3 overlap, and no warp ever waits at a CTA-wide barrier.  The lock-step kernel keeps the DMMA
 // pipe ~59 % busy (ncu, r01/r02): with all 16 warps in the same pass, each barrier interval
-// drains and refills the pipe.  Here the SM's warps always hold a mix of passes.
+// drains and refills the pipe.  Here the SM's warps always hold a mix of passes: 75 % DMMA pipe
+// (profiles/r02_fused5_256_sep_fused_summary.json), against a ceiling of the FP64 tensor pipe itself
+// (42.75 DMMAs per cell at 75 % column fill = 171 pipe cycles vs 153 cycles of HBM traffic per cell).
 //
 // Phases: the k-th use of a buffer waits for the k-th completion of its "full" barrier (parity
 // k & 1); a producer's first wait on an "empty" barrier passes at once (parity 1 on a fresh
